@@ -1,0 +1,17 @@
+"""B200-native (sm_100a) 2D swept-rule solver -- drop-in for the hot path of
+the reference ``sweptgrid`` engine (arXiv 2105.10332).
+
+Public API mirrors the reference (see api.py for the file:line mapping):
+``SolverConfig``, ``run(cfg) -> RunResult``, ``RunRecord.to_json()``,
+``substep`` (the equation plugin on device buffers), ``max_levels``,
+``build_schedule`` and the reference's exception types.
+"""
+from .api import (CudaError, FieldState, InvalidArgument, LinkModel, LogicError, NonPhysicalState, PoolSpec,
+                  RunRecord, RunResult, SnapshotIOError, Solver, SolverConfig, SweptError, TransportError,
+                  build_schedule, device_count, max_levels, plan_info, run, substep, version)
+
+__all__ = [
+    "CudaError", "FieldState", "InvalidArgument", "LinkModel", "LogicError", "NonPhysicalState", "PoolSpec",
+    "RunRecord", "RunResult", "SnapshotIOError", "Solver", "SolverConfig", "SweptError", "TransportError",
+    "build_schedule", "device_count", "max_levels", "plan_info", "run", "substep", "version",
+]

@@ -1,0 +1,566 @@
+// GPU engine -- see engine.hpp.
+#include "engine.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <string>
+
+namespace sg {
+
+cudaError_t launch_swept(int problem, const SweptArgs& a, int G, int threads, cudaStream_t s);
+cudaError_t launch_std(int problem, const StdArgs& a, cudaStream_t s);
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(SG_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class T>
+T* dev_alloc(DeviceCtx& d, std::size_t count) {
+    void* p = nullptr;
+    ck(cudaSetDevice(d.dev), "cudaSetDevice");
+    ck(cudaMalloc(&p, std::max<std::size_t>(count, 1) * sizeof(T)), "cudaMalloc");
+    d.allocs.push_back(p);
+    return static_cast<T*>(p);
+}
+
+template <class T>
+T* dev_upload(DeviceCtx& d, const std::vector<T>& v) {
+    T* p = dev_alloc<T>(d, v.size());
+    if (!v.empty()) ck(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+    return p;
+}
+
+}  // namespace
+
+Solver::Solver(const sg_config& cfg) : cfg_(cfg) {
+    const auto t0 = std::chrono::steady_clock::now();
+    setup_ = make_setup(cfg_);
+    const Equation& eq = setup_.eq;
+    px_ = cfg_.px;
+    py_ = cfg_.py;
+    if (px_ <= 0 && py_ <= 0) {
+        px_ = cfg_.ranks;
+        py_ = 1;
+    }
+    if (px_ <= 0) px_ = 1;
+    if (py_ <= 0) py_ = 1;
+    nparts_ = px_ * py_;
+    if (nparts_ > kMaxParts) fail(SG_EINVAL, "config: too many partitions");
+    pw_ = setup_.nx / px_;
+    ph_ = setup_.ny / py_;
+
+    int ndev = 0;
+    ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    if (ndev < 1) fail(SG_ECUDA, "no CUDA device visible (the GPU solver has no CPU fallback)");
+    int use = cfg_.devices > 0 ? std::min(cfg_.devices, ndev) : ndev;
+    use = std::min(use, nparts_);
+    devs_.resize(use);
+    for (int d = 0; d < use; ++d) {
+        devs_[d].dev = d;
+        ck(cudaSetDevice(d), "cudaSetDevice");
+        ck(cudaStreamCreateWithFlags(&devs_[d].stream, cudaStreamNonBlocking), "stream");
+        ck(cudaEventCreate(&devs_[d].ev_start), "event");
+        ck(cudaEventCreate(&devs_[d].ev_stop), "event");
+        ck(cudaEventCreateWithFlags(&devs_[d].ev_sync, cudaEventDisableTiming), "event");
+        devs_[d].d_err = dev_alloc<int>(devs_[d], 1);
+        for (int e = 0; e < use; ++e)
+            if (e != d) {
+                int can = 0;
+                cudaDeviceCanAccessPeer(&can, d, e);
+                if (can) {
+                    cudaError_t r = cudaDeviceEnablePeerAccess(e, 0);
+                    if (r != cudaSuccess && r != cudaErrorPeerAccessAlreadyEnabled)
+                        ck(r, "cudaDeviceEnablePeerAccess");
+                    cudaGetLastError();
+                }
+            }
+    }
+    parts_.resize(nparts_);
+    for (int p = 0; p < nparts_; ++p) {
+        parts_[p].id = p;
+        parts_[p].pi = p % px_;
+        parts_[p].pj = p / px_;
+        // contiguous blocks of partitions per device
+        parts_[p].dev = static_cast<int>(static_cast<long>(p) * use / nparts_);
+        devs_[parts_[p].dev].parts.push_back(p);
+    }
+
+    if (cfg_.engine == SG_SWEPT) {
+        const int k = max_levels(cfg_.block, eq.halo);
+        long flat = 0;
+        const long m = schedule_octahedra(cfg_.steps, k, eq.substeps, &flat);
+        actual_steps_ = flat / eq.substeps;
+        total_levels_ = flat;
+        final_level_ = actual_steps_ * eq.substeps;  // engine.cpp:518
+        plan_ = compile_swept_plan(cfg_.block, eq, m, final_level_);
+        for (const Launch& l : plan_.launches)
+            cell_updates_ += static_cast<long long>(plan_.updates_per_kind[l.kind]) *
+                             (setup_.nx / cfg_.block) * (setup_.ny / cfg_.block);
+        build_swept();
+    } else {
+        actual_steps_ = cfg_.steps;
+        total_levels_ = cfg_.steps * eq.substeps;
+        final_level_ = total_levels_;
+        cell_updates_ = total_levels_ * static_cast<long long>(setup_.nx) * setup_.ny;
+        build_standard();
+    }
+    for (auto& d : devs_) {
+        ck(cudaSetDevice(d.dev), "cudaSetDevice");
+        ck(cudaDeviceSynchronize(), "setup sync");
+    }
+    setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+Solver::~Solver() {
+    for (auto& d : devs_) {
+        cudaSetDevice(d.dev);
+        cudaStreamSynchronize(d.stream);
+        for (void* p : d.allocs) cudaFree(p);
+        for (auto e : d.prof_ev) cudaEventDestroy(e);
+        cudaEventDestroy(d.ev_start);
+        cudaEventDestroy(d.ev_stop);
+        cudaEventDestroy(d.ev_sync);
+        cudaStreamDestroy(d.stream);
+    }
+}
+
+void Solver::build_swept() {
+    const SweptPlan& P = plan_;
+    const int nv = setup_.eq.nvars;
+    const int b = cfg_.block;
+    const int pbx = pw_ / b, pby = ph_ / b;
+    const int g = P.ghost, extw = pbx + 2 * g, exth = pby + 2 * g;
+    const std::size_t rec_len = static_cast<std::size_t>(extw) * exth * nv * P.max_epad;
+    const std::size_t plane = static_cast<std::size_t>(pw_) * ph_;
+
+    // instances per CTA: keep ~<= 48 KB of smem per CTA, 1..8 instances
+    int inst_smem = 0;
+    for (int kd = 0; kd < K_NKINDS; ++kd) inst_smem = std::max(inst_smem, P.kinds[kd].smem_doubles * 8);
+    G_ = std::max(1, std::min(8, (48 * 1024) / std::max(1, inst_smem)));
+    if (inst_smem * G_ > 200 * 1024) fail(SG_EINVAL, "swept: block too large for on-chip phases");
+    threads_ = 128;
+
+    for (auto& pb : parts_) {
+        DeviceCtx& d = devs_[pb.dev];
+        pb.init = dev_alloc<double>(d, plane * nv);
+        pb.out = dev_alloc<double>(d, plane * nv);
+        pb.rec.resize(P.nslots);
+        for (int s = 0; s < P.nslots; ++s) pb.rec[s] = dev_alloc<double>(d, std::max<std::size_t>(rec_len, 1));
+        // level-0 piece of this partition (engine.cpp:199-209 load_initial)
+        std::vector<double> piece(plane * nv);
+        for (int v = 0; v < nv; ++v)
+            for (int y = 0; y < ph_; ++y)
+                std::memcpy(&piece[(static_cast<std::size_t>(v) * ph_ + y) * pw_],
+                            &setup_.initial[(static_cast<std::size_t>(v) * setup_.ny + pb.pj * ph_ + y) * setup_.nx +
+                                            pb.pi * pw_],
+                            sizeof(double) * pw_);
+        ck(cudaMemcpy(pb.init, piece.data(), piece.size() * sizeof(double), cudaMemcpyHostToDevice), "init H2D");
+    }
+    // ledger: record pushes across partition boundaries (P2P / NVLink stores)
+    long pushes = 0;
+    for (const auto& pb : parts_)
+        for (int bj = 0; bj < pby; ++bj)
+            for (int bi = 0; bi < pbx; ++bi)
+                for (int ej = -1; ej <= 1; ++ej)
+                    for (int ei = -1; ei <= 1; ++ei) {
+                        if (!ei && !ej) continue;
+                        const int tbi = bi - ei * pbx, tbj = bj - ej * pby;
+                        if (tbi < -g || tbi >= pbx + g || tbj < -g || tbj >= pby + g) continue;
+                        const int tp = ((pb.pj + ej + py_) % py_) * px_ + (pb.pi + ei + px_) % px_;
+                        if (tp != pb.id) ++pushes;
+                    }
+    for (const Launch& l : P.launches) {
+        if (P.kinds[l.kind].epad == 0) continue;
+        bytes_ += static_cast<long long>(pushes) * P.kinds[l.kind].exp_cells.size() * nv * 8;
+        if (pushes) messages_ += nparts_;
+    }
+
+    for (auto& d : devs_) {
+        ck(cudaSetDevice(d.dev), "cudaSetDevice");
+        for (int kd = 0; kd < K_NKINDS; ++kd) {
+            const KindLayout& K = P.kinds[kd];
+            if (K.nlev > kMaxLevels - 2) fail(SG_EINVAL, "swept: too many levels per phase");
+            std::vector<DevLevel> lv;
+            for (const PlanLevel& pl : K.lev)
+                lv.push_back({pl.bbox.x0, pl.bbox.y0, pl.bbox.w(), pl.bbox.h(), pl.off, pl.vstride, pl.comp.x0,
+                              pl.comp.x1, pl.comp.y0, pl.comp.y1});
+            d.d_lev[kd] = dev_upload(d, lv);
+            d.d_exp_off[kd] = dev_upload(d, K.exp_off);
+            d.d_exp_vs[kd] = dev_upload(d, K.exp_vstride);
+        }
+        for (const ClassTab& T : P.classes) {
+            std::vector<int4> im, in;
+            for (const Import& x : T.imports) im.push_back(make_int4(x.seg, x.src, x.dst, x.vstride));
+            for (const InitImport& x : T.inits) in.push_back(make_int4(x.rx, x.ry, x.dst, x.vstride));
+            d.d_imp.push_back(dev_upload(d, im));
+            d.d_init.push_back(dev_upload(d, in));
+        }
+        std::vector<double*> rt(static_cast<std::size_t>(nparts_) * P.nslots);
+        std::vector<const double*> it(nparts_);
+        std::vector<double*> ot(nparts_);
+        for (const auto& pb : parts_) {
+            for (int s = 0; s < P.nslots; ++s) rt[pb.id * P.nslots + s] = pb.rec[s];
+            it[pb.id] = pb.init;
+            ot[pb.id] = pb.out;
+        }
+        d.d_rec_tab = dev_upload(d, rt);
+        d.d_init_tab = dev_upload(d, it);
+        d.d_out_tab = dev_upload(d, ot);
+
+        for (std::size_t li = 0; li < P.launches.size(); ++li) {
+            const Launch& L = P.launches[li];
+            const KindLayout& K = P.kinds[L.kind];
+            const ClassTab& T = P.classes[L.cls];
+            SweptArgs a;
+            std::memset(&a, 0, sizeof a);
+            a.nlev = K.nlev;
+            a.rmin = K.rmin;
+            a.smem_doubles = K.smem_doubles;
+            a.nexp = static_cast<int>(K.exp_cells.size());
+            a.epad = K.epad;
+            a.lev = d.d_lev[L.kind];
+            a.exp_off = d.d_exp_off[L.kind];
+            a.exp_vs = d.d_exp_vs[L.kind];
+            a.imports = d.d_imp[L.cls];
+            a.nimp = static_cast<int>(T.imports.size());
+            a.inits = d.d_init[L.cls];
+            a.ninit = static_cast<int>(T.inits.size());
+            if (T.segs.size() > static_cast<std::size_t>(kMaxSegs)) fail(SG_ELOGIC, "swept: too many segments");
+            for (std::size_t s = 0; s < T.segs.size(); ++s) {
+                const long pl = static_cast<long>(li) - T.segs[s].delta;
+                if (pl < 0 || P.launches[pl].slot < 0) fail(SG_ELOGIC, "swept: import from a launch without record");
+                a.segs[s] = {P.launches[pl].slot, T.segs[s].di, T.segs[s].dj, P.kinds[T.segs[s].pkind].epad};
+            }
+            a.nsegs = static_cast<int>(T.segs.size());
+            a.frame = L.frame;
+            a.stage0 = L.stage0;
+            a.r_out = L.r_out;
+            a.my_slot = L.slot < 0 ? 0 : L.slot;
+            a.b = b;
+            a.nx = setup_.nx;
+            a.ny = setup_.ny;
+            a.pw = pw_;
+            a.ph = ph_;
+            a.pbx = pbx;
+            a.pby = pby;
+            a.px = px_;
+            a.py = py_;
+            a.ghost = g;
+            a.extw = extw;
+            a.nslots = P.nslots;
+            a.ndev_parts = static_cast<int>(d.parts.size());
+            for (std::size_t q = 0; q < d.parts.size(); ++q) a.dev_parts[q] = d.parts[q];
+            a.rec = d.d_rec_tab;
+            a.init_planes = d.d_init_tab;
+            a.out_planes = d.d_out_tab;
+            if (setup_.eq.problem == SG_HEAT) {
+                a.c0 = setup_.heat_fx;
+                a.c1 = setup_.heat_fy;
+            } else {
+                a.c0 = setup_.gamma;
+                a.c1 = setup_.cx_pred;
+                a.c2 = setup_.cy_pred;
+                a.c3 = setup_.cx_corr;
+                a.c4 = setup_.cy_corr;
+            }
+            a.err = d.d_err;
+            d.swept_args.push_back(a);
+        }
+    }
+    prof_kind_ = P.m > 0 ? K_OCT : K_UP;
+}
+
+void Solver::build_standard() {
+    const Equation& eq = setup_.eq;
+    const int n = eq.halo, nv = eq.nvars, S = eq.substeps;
+    const int pitch = pw_ + 2 * n, rows = ph_ + 2 * n;
+    const std::size_t gplane = static_cast<std::size_t>(pitch) * rows;
+    for (auto& pb : parts_) {
+        DeviceCtx& d = devs_[pb.dev];
+        pb.ring.resize(S + 1);
+        for (int s = 0; s <= S; ++s) pb.ring[s] = dev_alloc<double>(d, gplane * nv);
+        pb.init_ghosted = dev_alloc<double>(d, gplane * nv);
+        // ghosted level-0 piece, ghosts from the periodic neighbours (cross only)
+        std::vector<double> piece(gplane * nv, 0.0);
+        for (int v = 0; v < nv; ++v)
+            for (int y = -n; y < ph_ + n; ++y)
+                for (int x = -n; x < pw_ + n; ++x) {
+                    const bool inx = x >= 0 && x < pw_, iny = y >= 0 && y < ph_;
+                    if (!inx && !iny) continue;  // corners are never read
+                    const int gx = ((pb.pi * pw_ + x) % setup_.nx + setup_.nx) % setup_.nx;
+                    const int gy = ((pb.pj * ph_ + y) % setup_.ny + setup_.ny) % setup_.ny;
+                    piece[(static_cast<std::size_t>(v) * rows + (y + n)) * pitch + (x + n)] =
+                        setup_.initial[(static_cast<std::size_t>(v) * setup_.ny + gy) * setup_.nx + gx];
+                }
+        ck(cudaMemcpy(pb.init_ghosted, piece.data(), piece.size() * sizeof(double), cudaMemcpyHostToDevice),
+           "init H2D");
+    }
+    for (auto& d : devs_) {
+        ck(cudaSetDevice(d.dev), "cudaSetDevice");
+        for (int phase = 0; phase <= S; ++phase) {
+            // level L with L % (S+1) == phase
+            std::vector<const double*> r1(nparts_), r2(nparts_);
+            std::vector<double*> o(nparts_);
+            for (const auto& pb : parts_) {
+                r1[pb.id] = pb.ring[(phase + S) % (S + 1)];
+                r2[pb.id] = pb.ring[(phase + S - 1 + (S + 1)) % (S + 1)];
+                o[pb.id] = pb.ring[phase];
+            }
+            d.d_std_r1.push_back(dev_upload(d, r1));
+            d.d_std_r2.push_back(dev_upload(d, r2));
+            d.d_std_out.push_back(dev_upload(d, o));
+        }
+    }
+    // ledger: 4 face strips per partition per level when neighbours differ
+    for (long l = 1; l <= final_level_; ++l)
+        for (const auto& pb : parts_) {
+            if (px_ > 1) {
+                messages_ += 2;
+                bytes_ += 2LL * ph_ * n * nv * 8;
+            }
+            if (py_ > 1) {
+                messages_ += 2;
+                bytes_ += 2LL * pw_ * n * nv * 8;
+            }
+            (void)pb;
+        }
+    prof_kind_ = 100;  // std step
+}
+
+void Solver::reset() {
+    for (auto& d : devs_) {
+        ck(cudaSetDevice(d.dev), "cudaSetDevice");
+        ck(cudaMemsetAsync(d.d_err, 0, sizeof(int), d.stream), "memset");
+    }
+    if (cfg_.engine == SG_STANDARD) {
+        const Equation& eq = setup_.eq;
+        const std::size_t gplane =
+            static_cast<std::size_t>(pw_ + 2 * eq.halo) * (ph_ + 2 * eq.halo) * eq.nvars;
+        for (auto& pb : parts_) {
+            DeviceCtx& d = devs_[pb.dev];
+            ck(cudaSetDevice(d.dev), "cudaSetDevice");
+            ck(cudaMemcpyAsync(pb.ring[0], pb.init_ghosted, gplane * sizeof(double), cudaMemcpyDeviceToDevice,
+                               d.stream),
+               "reset");
+        }
+    }
+}
+
+double Solver::solve() {
+    const bool multi = devs_.size() > 1;
+    const int prob = setup_.eq.problem;
+    launches_ = 0;
+    prof_seconds_ = 0.0;
+    prof_launches_ = 0;
+    prof_bytes_ = 0.0;
+    prof_updates_ = 0.0;
+    DeviceCtx& d0 = devs_[0];
+    std::size_t prof_i = 0;
+    auto prof_begin = [&](bool on) -> cudaEvent_t {
+        if (!on) return nullptr;
+        if (prof_i + 2 > d0.prof_ev.size()) {
+            cudaEvent_t a, c;
+            cudaSetDevice(d0.dev);
+            ck(cudaEventCreate(&a), "event");
+            ck(cudaEventCreate(&c), "event");
+            d0.prof_ev.push_back(a);
+            d0.prof_ev.push_back(c);
+        }
+        cudaEvent_t e = d0.prof_ev[prof_i];
+        ck(cudaEventRecord(e, d0.stream), "event");
+        return e;
+    };
+    auto prof_end = [&](bool on) {
+        if (!on) return;
+        ck(cudaEventRecord(d0.prof_ev[prof_i + 1], d0.stream), "event");
+        prof_i += 2;
+    };
+    // barrier between dependent launches on different GPUs
+    auto cross_sync = [&]() {
+        if (!multi) return;
+        for (auto& d : devs_) {
+            cudaSetDevice(d.dev);
+            ck(cudaEventRecord(d.ev_sync, d.stream), "event");
+        }
+        for (auto& d : devs_)
+            for (auto& e : devs_)
+                if (&d != &e) ck(cudaStreamWaitEvent(d.stream, e.ev_sync, 0), "wait");
+    };
+    for (auto& d : devs_) {
+        cudaSetDevice(d.dev);
+        ck(cudaEventRecord(d.ev_start, d.stream), "event");
+    }
+    if (cfg_.engine == SG_SWEPT) {
+        for (std::size_t li = 0; li < plan_.launches.size(); ++li) {
+            const bool pr = profile && plan_.launches[li].kind == prof_kind_;
+            for (auto& d : devs_) {
+                if (multi) cudaSetDevice(d.dev);
+                if (&d == &d0) prof_begin(pr);
+                ck(launch_swept(prob, d.swept_args[li], G_, threads_, d.stream), "swept launch");
+                if (&d == &d0) prof_end(pr);
+                ++launches_;
+            }
+            if (pr) {
+                ++prof_launches_;
+                const Launch& L = plan_.launches[li];
+                const ClassTab& T = plan_.classes[L.cls];
+                const double inst = static_cast<double>(pw_ / cfg_.block) * (ph_ / cfg_.block) *
+                                    devs_[0].parts.size();
+                prof_bytes_ += inst * (T.imports.size() + T.inits.size() + plan_.kinds[L.kind].exp_cells.size()) *
+                               setup_.eq.nvars * 8.0;
+                prof_updates_ += inst * plan_.updates_per_kind[L.kind];
+            }
+            cross_sync();
+        }
+    } else {
+        const Equation& eq = setup_.eq;
+        const int S = eq.substeps;
+        for (long l = 1; l <= final_level_; ++l) {
+            const int phase = static_cast<int>(l % (S + 1));
+            const int stage = static_cast<int>((l - 1) % S);
+            const bool pr = profile;
+            for (auto& d : devs_) {
+                if (multi) cudaSetDevice(d.dev);
+                StdArgs a;
+                std::memset(&a, 0, sizeof a);
+                a.nvars = eq.nvars;
+                a.n = eq.halo;
+                a.pw = pw_;
+                a.ph = ph_;
+                a.px = px_;
+                a.py = py_;
+                a.pitch = pw_ + 2 * eq.halo;
+                a.rows = ph_ + 2 * eq.halo;
+                a.stage = stage;
+                a.ndev_parts = static_cast<int>(d.parts.size());
+                for (std::size_t q = 0; q < d.parts.size(); ++q) a.dev_parts[q] = d.parts[q];
+                a.read1 = d.d_std_r1[phase];
+                a.read2 = l >= 2 ? d.d_std_r2[phase] : d.d_std_r1[phase];
+                a.out = d.d_std_out[phase];
+                if (eq.problem == SG_HEAT) {
+                    a.c0 = setup_.heat_fx;
+                    a.c1 = setup_.heat_fy;
+                } else {
+                    a.c0 = setup_.gamma;
+                    a.c1 = stage == 0 ? setup_.cx_pred : setup_.cx_corr;
+                    a.c2 = stage == 0 ? setup_.cy_pred : setup_.cy_corr;
+                }
+                a.err = d.d_err;
+                if (&d == &d0) prof_begin(pr);
+                ck(launch_std(eq.problem, a, d.stream), "std launch");
+                if (&d == &d0) prof_end(pr);
+                ++launches_;
+            }
+            if (pr) {
+                ++prof_launches_;
+                const double cells = static_cast<double>(pw_) * ph_ * devs_[0].parts.size();
+                // heat: read 8 + write 8; euler: predictor 64, corrector 96
+                const double bpu = eq.problem == SG_HEAT ? 16.0 : (stage == 0 ? 64.0 : 96.0);
+                prof_bytes_ += cells * bpu;
+                prof_updates_ += cells;
+            }
+            cross_sync();
+        }
+    }
+    double worst = 0.0;
+    for (auto& d : devs_) {
+        cudaSetDevice(d.dev);
+        ck(cudaEventRecord(d.ev_stop, d.stream), "event");
+    }
+    for (auto& d : devs_) {
+        cudaSetDevice(d.dev);
+        ck(cudaEventSynchronize(d.ev_stop), "solve");
+        float ms = 0.f;
+        ck(cudaEventElapsedTime(&ms, d.ev_start, d.ev_stop), "elapsed");
+        worst = std::max(worst, ms * 1e-3);
+    }
+    for (std::size_t i = 0; i + 1 < prof_i; i += 2) {
+        float ms = 0.f;
+        ck(cudaEventElapsedTime(&ms, d0.prof_ev[i], d0.prof_ev[i + 1]), "elapsed");
+        prof_seconds_ += ms * 1e-3;
+    }
+    last_solve_ = worst;
+    check_error();
+    return worst;
+}
+
+void Solver::check_error() {
+    for (auto& d : devs_) {
+        int e = 0;
+        cudaSetDevice(d.dev);
+        ck(cudaMemcpy(&e, d.d_err, sizeof(int), cudaMemcpyDeviceToHost), "err D2H");
+        if (e) fail(SG_ENONPHYS, "non-physical state: rho <= 0 or p <= 0");
+    }
+}
+
+void Solver::fetch(sg_result* r) {
+    const Equation& eq = setup_.eq;
+    const int nv = eq.nvars;
+    const std::size_t nx = setup_.nx, ny = setup_.ny;
+    double* field = static_cast<double*>(std::malloc(sizeof(double) * nv * nx * ny));
+    if (!field) fail(SG_ELOGIC, "out of host memory");
+    std::vector<double> piece;
+    for (auto& pb : parts_) {
+        DeviceCtx& d = devs_[pb.dev];
+        cudaSetDevice(d.dev);
+        if (cfg_.engine == SG_SWEPT) {
+            piece.resize(static_cast<std::size_t>(pw_) * ph_ * nv);
+            ck(cudaMemcpy(piece.data(), pb.out, piece.size() * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+            for (int v = 0; v < nv; ++v)
+                for (int y = 0; y < ph_; ++y)
+                    std::memcpy(&field[(v * ny + pb.pj * ph_ + y) * nx + pb.pi * pw_],
+                                &piece[(static_cast<std::size_t>(v) * ph_ + y) * pw_], sizeof(double) * pw_);
+        } else {
+            const int n = eq.halo, pitch = pw_ + 2 * n, rows = ph_ + 2 * n;
+            piece.resize(static_cast<std::size_t>(pitch) * rows * nv);
+            const double* src = pb.ring[final_level_ % (eq.substeps + 1)];
+            ck(cudaMemcpy(piece.data(), src, piece.size() * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+            for (int v = 0; v < nv; ++v)
+                for (int y = 0; y < ph_; ++y)
+                    std::memcpy(&field[(v * ny + pb.pj * ph_ + y) * nx + pb.pi * pw_],
+                                &piece[(static_cast<std::size_t>(v) * rows + y + n) * pitch + n], sizeof(double) * pw_);
+        }
+    }
+    std::memset(r, 0, sizeof *r);
+    r->engine = cfg_.engine;
+    r->problem = cfg_.problem;
+    r->mode = cfg_.mode;
+    r->nx = setup_.nx;
+    r->ny = setup_.ny;
+    r->block = cfg_.block;
+    r->ranks = cfg_.ranks;
+    r->px = px_;
+    r->py = py_;
+    r->nvars = nv;
+    r->steps_requested = cfg_.steps;
+    r->actual_steps = actual_steps_;
+    r->total_levels = total_levels_;
+    if (cfg_.engine == SG_SWEPT) {
+        r->octahedra = plan_.m;
+        r->communicates = plan_.m + 1;
+    }
+    r->final_level = final_level_;
+    r->dt = setup_.dt;
+    r->dx = setup_.dx;
+    r->dy = setup_.dy;
+    r->setup_seconds = setup_seconds;
+    r->solve_seconds = last_solve_;
+    r->messages = messages_;
+    r->bytes = bytes_;
+    r->cell_updates = cell_updates_;
+    r->kernel_launches = launches_;
+    r->final_field = field;
+}
+
+void Solver::kernel_stats(int which, double* seconds, long* launches, double* alg_bytes, double* updates) const {
+    (void)which;
+    if (seconds) *seconds = prof_seconds_;
+    if (launches) *launches = prof_launches_;
+    if (alg_bytes) *alg_bytes = prof_bytes_;
+    if (updates) *updates = prof_updates_;
+}
+
+}  // namespace sg

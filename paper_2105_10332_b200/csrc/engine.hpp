@@ -1,0 +1,88 @@
+// GPU engine: partitions, device buffers and the solve loops for the swept
+// and standard engines (the B200 replacement of SweptRank / StandardRank,
+// engine.cpp:169-425 of the reference).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <vector>
+
+#include "kernels.cuh"
+#include "plan.hpp"
+#include "sg_internal.hpp"
+
+namespace sg {
+
+struct PartBuffers {
+    int id = 0, pi = 0, pj = 0, dev = 0;
+    // swept
+    double* init = nullptr;             // [var][ph][pw] level-0 piece
+    double* out = nullptr;              // [var][ph][pw] output level piece
+    std::vector<double*> rec;           // [nslots] records, ghost-extended instance grid
+    // standard
+    std::vector<double*> ring;          // [S+1] ghosted planes
+    double* init_ghosted = nullptr;     // resident ghosted copy of level 0
+};
+
+struct DeviceCtx {
+    int dev = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev_start = nullptr, ev_stop = nullptr, ev_sync = nullptr;
+    int* d_err = nullptr;
+    std::vector<int> parts;
+    // device-resident tables
+    std::vector<void*> allocs;
+    DevLevel* d_lev[K_NKINDS] = {};
+    int* d_exp_off[K_NKINDS] = {};
+    int* d_exp_vs[K_NKINDS] = {};
+    std::vector<int4*> d_imp, d_init;
+    double** d_rec_tab = nullptr;
+    const double** d_init_tab = nullptr;
+    double** d_out_tab = nullptr;
+    std::vector<const double**> d_std_r1, d_std_r2;
+    std::vector<double**> d_std_out;
+    // per-launch arguments (swept) -- built once at create
+    std::vector<SweptArgs> swept_args;
+    std::vector<cudaEvent_t> prof_ev;   // kernel profiling pairs
+};
+
+class Solver {
+  public:
+    explicit Solver(const sg_config& cfg);
+    ~Solver();
+    void reset();
+    double solve();  // device seconds (max over devices)
+    void fetch(sg_result* r);
+    void kernel_stats(int which, double* seconds, long* launches, double* alg_bytes, double* updates) const;
+
+    const Setup& setup() const { return setup_; }
+    double setup_seconds = 0.0;
+    bool profile = false;
+
+  private:
+    void build_swept();
+    void build_standard();
+    void check_error();
+
+    sg_config cfg_;
+    Setup setup_;
+    SweptPlan plan_;
+    int px_ = 1, py_ = 1, pw_ = 0, ph_ = 0, nparts_ = 1;
+    long final_level_ = 0, total_levels_ = 0, actual_steps_ = 0;
+    long long cell_updates_ = 0;
+    long messages_ = 0;
+    long long bytes_ = 0;
+    long launches_ = 0;
+    int G_ = 1, threads_ = 128;
+    std::vector<PartBuffers> parts_;
+    std::vector<DeviceCtx> devs_;
+    double last_solve_ = 0.0;
+    // profiling of the dominant kernel class
+    int prof_kind_ = -1;
+    double prof_seconds_ = 0.0;
+    long prof_launches_ = 0;
+    double prof_bytes_ = 0.0, prof_updates_ = 0.0;
+};
+
+}  // namespace sg

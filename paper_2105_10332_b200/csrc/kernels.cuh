@@ -1,0 +1,66 @@
+// Kernel argument structures shared by kernels.cu and engine.cpp.
+#pragma once
+
+#include <cstdint>
+
+namespace sg {
+
+constexpr int kMaxLevels = 40;   // relative levels per kind (2k + 2 <= 40 -> b <= 36 heat)
+constexpr int kMaxSegs = 24;
+constexpr int kMaxParts = 64;
+
+struct DevLevel {
+    int bx0, by0, bw, bh;   // resident bounding box
+    int off, vstride;       // smem offset of var 0 / per-var stride
+    int cx0, cx1, cy0, cy1; // computed rect (empty for r <= 0)
+};
+
+struct DevSeg {
+    int slot;   // record slot of the producer launch
+    int di, dj;
+    int epad;   // producer record length
+};
+
+// One swept phase launch (all partitions resident on one device).
+struct SweptArgs {
+    // kind layout
+    int nlev, rmin, smem_doubles, nexp, epad;
+    const DevLevel* lev;     // [nlev - rmin + 1]
+    const int* exp_off;      // [nexp]
+    const int* exp_vs;       // [nexp]
+    // class tables
+    const int4* imports;     // {seg, src, dst, vstride}
+    int nimp;
+    const int4* inits;       // {rx, ry, dst, vstride}
+    int ninit;
+    DevSeg segs[kMaxSegs];
+    int nsegs;
+    // launch
+    int frame, stage0, r_out, my_slot;
+    // geometry
+    int b, nx, ny, pw, ph, pbx, pby, px, py, ghost, extw, nslots;
+    int ndev_parts;
+    int dev_parts[kMaxParts];        // partitions handled by this launch
+    double* const* rec;              // [part * nslots + slot]
+    const double* const* init_planes;// [part] [var][ph][pw]
+    double* const* out_planes;       // [part] [var][ph][pw]
+    double c0, c1, c2, c3;           // heat: fx, fy | euler: gamma, cx, cy (per stage)
+    double c4, c5;
+    int* err;
+};
+
+// One standard sub-step (all partitions on one device); planes carry a
+// ghost frame of width n: pitch = pw + 2n, rows = ph + 2n.
+struct StdArgs {
+    int nvars, n, pw, ph, px, py, pitch, rows;
+    int stage;
+    int ndev_parts;
+    int dev_parts[kMaxParts];
+    const double* const* read1;   // [part] level-1 plane (ghosted)
+    const double* const* read2;   // [part] level-2 plane (corrector base)
+    double* const* out;           // [part] level plane (ghosted, pushes into neighbours)
+    double c0, c1, c2, c3;
+    int* err;
+};
+
+}  // namespace sg
