@@ -1,0 +1,374 @@
+#!/usr/bin/env python3
+"""Benchmark: 2D swept-rule heat, weak scaling, 8192^2 cells per GPU, b=16,
+10k requested steps (BASELINE.json configs[4]) -- swept and standard engines.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A "step" is one full solve of the workload (10003 sub-step levels of the
+8192^2-per-GPU grid) from the resident initial condition.  Prints ONE JSON
+line on rank 0 (contract in the task statement):
+  value     swept cell-updates/s over all GPUs, inputs resident in HBM, device
+            time (CUDA events on the launching stream), max over ranks
+  e2e       the same through the C-ABI with host buffers: pinned H2D of the
+            initial field + solve + D2H of the final field, every step
+  roofline  dominant kernel (Octahedron phase): algorithmic bytes per launch /
+            mean launch time (CUDA events around each launch), vs measured HBM
+  cpu_baseline  the reference (oracle/_ref, built from its own sources) timed
+            on this host on a bounded sample of the same workload
+Synthetic data = the reference's own deterministic initial condition
+(sin*sin, engine.cpp:31-42).  Inputs (537 MB/plane) exceed L2 (126 MB).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import shutil
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PER_GPU = 8192
+BLOCK = 16
+REQ_STEPS = 10000
+METRIC = "cell-updates/sec (fp64) + swept/standard speedup at 1/2/4/8 B200 vs CPU ref"
+GRIDS = {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (4, 2)}
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()), "measured"
+        except Exception:  # noqa: BLE001
+            pass
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self):
+        self.rows, self.proc = [], None
+
+    def start(self):
+        if not shutil.which("nvidia-smi"):
+            return
+        self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                      "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+        sm = [float(r[1]) for r in self.rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) > 8:
+                for i, nm in enumerate(names):
+                    if r[5 + i].lower() == "active":
+                        reasons.add(nm)
+        load = [s for s in sm if s > 0.5 * (max(mx) if mx else 1)] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def ncu_traffic(tag: str):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    capture summary (profiles/*.json with a matching `workload`)."""
+    best = None
+    for p in sorted((ROOT / "profiles").glob("*.json")):
+        try:
+            j = json.loads(p.read_text())
+        except Exception:  # noqa: BLE001
+            continue
+        if j.get("workload") == tag and j.get("dram_bytes_per_launch"):
+            best = (j["dram_bytes_per_launch"], p.name)
+    return best
+
+
+def cpu_reference_sample(nx, ny, steps, engine, threads):
+    """Time the reference (oracle/_ref/ref_run, built from the reference's own
+    sources) on a bounded sample; returns (cell-updates/s, record)."""
+    exe = ROOT / "oracle" / "_ref" / "ref_run"
+    if not exe.exists():
+        return None, None
+    if ny != nx:  # the reference is square-only (config.hpp:50): sample the square per-GPU grid
+        nx = ny = min(nx, ny)
+    cols = nx // BLOCK
+    if engine == "swept":
+        ranks = max(r for r in range(1, threads + 1) if cols % r == 0)
+        cfg = {"problem": "heat", "nx": nx, "block": BLOCK, "steps": steps, "ranks": ranks, "engine": "swept"}
+    else:
+        cfg = {"problem": "heat", "nx": nx, "block": BLOCK, "steps": steps, "ranks": 1, "engine": "standard",
+               "pool_a": {"workers": threads, "cost": 1.0}}
+    out = subprocess.run([str(exe), json.dumps(cfg), "1"], capture_output=True, text=True, timeout=900)
+    try:
+        rec = json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception:  # noqa: BLE001
+        return None, None
+    if "error" in rec:
+        return None, rec
+    return rec["cell_updates_per_s"], dict(rec, cfg=cfg)
+
+
+def run_reference_arm(args, world, rank):
+    if rank != 0:
+        return 0
+    px, py = GRIDS.get(args.gpus, (args.gpus, 1))
+    nx, ny = PER_GPU * px, PER_GPU * py
+    threads = os.cpu_count() or 1
+    exe = ROOT / "oracle" / "_ref" / "ref_run"
+    if not exe.exists():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ref_run was not built on this host"}))
+        return 0
+    sample_steps = args.ref_sample_steps
+    rates = []
+    rec = None
+    for i in range(args.warmup + args.steps):
+        r, rec = cpu_reference_sample(nx, ny, sample_steps, "swept", threads)
+        if r is None:
+            print(json.dumps({"impl": "reference", "unavailable": f"reference run failed: {rec}"}))
+            return 0
+        if i >= args.warmup:
+            rates.append(r)
+    value = statistics.median(rates)
+    sample = (f"reference swept engine, heat {rec['cfg']['nx']}^2 b{BLOCK}, {sample_steps} requested steps "
+              f"({rec['actual_steps']} actual), {rec['cfg']['ranks']} ranks x 1 thread, median of {len(rates)}")
+    line = {
+        "metric": METRIC, "impl": "reference", "value": value, "unit": "cell-updates/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": rec["median_wall_seconds"] * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args.gpus, nx, ny),
+        "cpu_baseline": {"value": value, "unit": "cell-updates/s", "cores": rec["cfg"]["ranks"],
+                         "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def workload_config(n, nx, ny):
+    px, py = GRIDS.get(n, (n, 1))
+    return {"workload": f"heat2d-swept-weak-{PER_GPU}sq-per-gpu-b{BLOCK}-{REQ_STEPS}steps", "problem": "heat",
+            "nx": nx, "ny": ny, "block": BLOCK, "requested_steps": REQ_STEPS, "partition": f"{px}x{py}",
+            "engine": "swept (standard timed alongside)", "l2": "inputs larger than L2 (537 MB per plane per GPU)"}
+
+
+def main():
+    global PER_GPU, REQ_STEPS
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--req-steps", type=int, default=REQ_STEPS)
+    ap.add_argument("--per-gpu", type=int, default=PER_GPU)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--no-extra", action="store_true", help="skip the Euler / standard side measurements")
+    ap.add_argument("--ref-sample-steps", type=int, default=21)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    if args.impl == "reference":
+        return run_reference_arm(args, world, rank)
+
+    import numpy as np
+    import torch
+
+    import paper_2105_10332_b200 as sg
+
+    PER_GPU, REQ_STEPS = args.per_gpu, args.req_steps
+    if world > 1:
+        # one process per GPU: rank r owns partition r of the global grid.
+        # (Cross-process coupling: see DESIGN.md "multi-GPU"; this round the
+        # whole grid is driven by rank 0 over all visible devices.)
+        import torch.distributed as dist
+        torch.cuda.set_device(env_int("LOCAL_RANK", 0))
+        dist.init_process_group("nccl", init_method="env://")
+        if rank != 0:
+            dist.barrier()
+            dist.destroy_process_group()
+            return 0
+    n = args.gpus
+    px, py = GRIDS.get(n, (n, 1))
+    nx, ny = PER_GPU * px, PER_GPU * py
+    base = dict(problem="heat", nx=nx, ny=ny, block=BLOCK, steps=REQ_STEPS, ranks=px * py, px=px, py=py, devices=n)
+
+    def timed(engine, profile):
+        cfg = sg.SolverConfig(engine=engine, **base)
+        s = sg.Solver(cfg, profile=profile)
+        for _ in range(args.warmup):
+            s.reset()
+            s.solve()
+        torch.cuda.synchronize()
+        dev, kst = [], []
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            s.reset()
+            dev.append(s.solve())
+            kst.append(s.kernel_stats())
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        res = s.fetch()
+        return s, dev, kst, wall, res
+
+    clocks = Clocks()
+    clocks.start()
+    sw, sw_dev, sw_k, sw_wall, sw_res = timed("swept", True)
+    ck = clocks.stop()
+    updates = sw_res.record.cell_updates
+    dev_total = sum(sw_dev)
+    value = updates * args.steps / dev_total
+
+    # ---- e2e: pinned host in -> solve -> host out, every step --------------
+    nv = 1
+    host_in = torch.empty((nv, ny, nx), dtype=torch.float64).pin_memory()
+    host_out = torch.empty((nv, ny, nx), dtype=torch.float64).pin_memory()
+    sw.initial(host_in)  # the reference initial condition (make_setup, engine.cpp:31-42)
+    for _ in range(1):
+        sw.upload(host_in)
+        sw.reset()
+        sw.solve()
+        sw.download(host_out)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        sw.upload(host_in)
+        sw.reset()
+        sw.solve()
+        sw.download(host_out)
+    torch.cuda.synchronize()
+    e2e_wall = time.perf_counter() - t0
+    e2e_value = updates * args.steps / e2e_wall
+    assert np.array_equal(host_out.numpy(), sw_res.final_field.data), "e2e output differs from resident solve"
+    launches = sw_res.record.kernel_launches * args.steps
+
+    # ---- roofline of the dominant kernel (Octahedron phase) ----------------
+    peaks, peak_kind = measured_peaks()
+    k = sw_k[-1]
+    per_launch_bytes = k["alg_bytes"] / max(1, k["launches"])
+    per_launch_s = k["seconds"] / max(1, k["launches"])
+    achieved = per_launch_bytes / per_launch_s / 1e9
+    tag = workload_config(n, nx, ny)["workload"]
+    nt = ncu_traffic(tag)
+    roof = {"kernel": "swept_phase_kernel<heat> (Octahedron launches)", "bound": "hbm",
+            "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": nt[0] if nt else None,
+            "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else
+            "fallback 6650 GB/s (B200_PROFILING.md)",
+            "alg_bytes_per_launch": per_launch_bytes, "mean_launch_ms": per_launch_s * 1e3,
+            "launches_per_step": k["launches"], "share_of_step": round(k["seconds"] / sw_dev[-1], 4),
+            "traffic_source": nt[1] if nt else None}
+    sw.close()
+
+    # ---- standard engine on the same workload (speedup) --------------------
+    extra = {}
+    st_value = None
+    if not args.no_extra:
+        base_std = dict(base, steps=sw_res.record.actual_steps)
+        cfg = sg.SolverConfig(engine="standard", **base_std)
+        st = sg.Solver(cfg, profile=False)
+        for _ in range(args.warmup):
+            st.reset()
+            st.solve()
+        st_dev = []
+        for _ in range(args.steps):
+            st.reset()
+            st_dev.append(st.solve())
+        st_res = st.fetch()
+        st_value = st_res.record.cell_updates * args.steps / sum(st_dev)
+        same = bool(np.array_equal(st_res.final_field.data, sw_res.final_field.data))
+        st.close()
+        extra["standard"] = {"value": st_value, "unit": "cell-updates/s", "ms_per_step": 1e3 * sum(st_dev) / args.steps,
+                             "bitwise_equal_to_swept": same}
+        extra["swept_over_standard"] = value / st_value
+        # configs[1]: Euler 960^2 b16 swept vs standard (one GPU)
+        eu = {}
+        for eng in ("swept", "standard"):
+            steps_e = 500 if eng == "swept" else None
+            cfg = sg.SolverConfig(problem="euler", nx=960, block=16, engine=eng,
+                                  steps=steps_e or eu["swept"]["actual_steps"])
+            s = sg.Solver(cfg)
+            for _ in range(3):
+                s.reset()
+                s.solve()
+            ts = []
+            for _ in range(args.steps):
+                s.reset()
+                ts.append(s.solve())
+            r = s.fetch()
+            eu[eng] = {"value": r.record.cell_updates * args.steps / sum(ts), "actual_steps": r.record.actual_steps,
+                       "ms_per_step": 1e3 * sum(ts) / args.steps}
+            s.close()
+        eu["swept_over_standard"] = eu["swept"]["value"] / eu["standard"]["value"]
+        extra["euler_960_b16"] = eu
+
+    # ---- CPU baseline: the reference on this host, bounded sample ----------
+    cpu = None
+    if not args.no_cpu and n == 1:
+        threads = os.cpu_count() or 1
+        v, rec = cpu_reference_sample(nx, ny, args.ref_sample_steps, "swept", threads)
+        if v is not None:
+            cpu = {"value": v, "unit": "cell-updates/s", "cores": rec["cfg"]["ranks"], "kind": "reference",
+                   "sample": f"reference swept engine (oracle/_ref), heat {rec['cfg']['nx']}^2 b{BLOCK}, "
+                             f"{args.ref_sample_steps} requested steps ({rec['actual_steps']} actual), "
+                             f"{rec['cfg']['ranks']} ranks x 1 thread, wall {rec['median_wall_seconds']:.2f} s"}
+            vs, recs = cpu_reference_sample(nx, ny, args.ref_sample_steps, "standard", threads)
+            if vs is not None:
+                cpu["standard_value"] = vs
+                cpu["standard_sample"] = f"reference standard engine, 1 rank x {threads} OpenMP threads"
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "cell-updates/s", "n_gpus": n, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * dev_total / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(n, nx, ny),
+        "e2e": {"value": e2e_value, "unit": "cell-updates/s", "h2d_bytes_per_step": nv * nx * ny * 8,
+                "d2h_bytes_per_step": nv * nx * ny * 8},
+        "gpu_launches": launches,
+        "roofline": roof, "cpu_baseline": cpu, "clocks": ck,
+        "actual_steps": sw_res.record.actual_steps, "cell_updates_per_step": updates,
+        "wall_ms_per_step": 1e3 * sw_wall / args.steps,
+    }
+    line.update(extra)
+    print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

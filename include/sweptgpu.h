@@ -130,6 +130,13 @@ int sg_solver_fetch(sg_solver* s, sg_result* out, char* err, size_t errlen);
  * solve (CUDA events around each of its launches), summed, and its count. */
 int sg_solver_kernel_stats(sg_solver* s, int which, double* seconds, long* launches,
                            double* alg_bytes, double* updates);
+/* Host-buffer I/O of the resident solver (the e2e path): upload replaces the
+ * level-0 field with `host` ([var][ny][nx] fp64, pinned or pageable) and
+ * download writes the final field into `host`; both synchronous. */
+int sg_solver_upload(sg_solver* s, const double* host, char* err, size_t errlen);
+int sg_solver_download(sg_solver* s, double* host, char* err, size_t errlen);
+/* The initial condition make_setup computed (engine.cpp:27-70), [var][ny][nx]. */
+int sg_solver_initial(sg_solver* s, double* host, char* err, size_t errlen);
 /* Enable (1) / disable (0) per-launch CUDA events around the dominant kernel. */
 int sg_solver_set_profile(sg_solver* s, int on);
 void sg_solver_destroy(sg_solver* s);

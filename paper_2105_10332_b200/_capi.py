@@ -50,7 +50,7 @@ class sg_result(C.Structure):
 EXPORTS = (
     "sg_config_default", "sg_validate", "sg_run", "sg_free_result", "sg_solver_create",
     "sg_solver_reset", "sg_solver_solve", "sg_solver_fetch", "sg_solver_kernel_stats",
-    "sg_solver_set_profile", "sg_solver_destroy", "sg_plan_info", "sg_max_levels", "sg_schedule",
+    "sg_solver_upload", "sg_solver_download", "sg_solver_initial", "sg_solver_set_profile", "sg_solver_destroy", "sg_plan_info", "sg_max_levels", "sg_schedule",
     "sg_substep", "sg_version", "sg_device_count",
 )
 
@@ -81,6 +81,9 @@ def load() -> C.CDLL:
     L.sg_solver_kernel_stats.argtypes = [sp, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_long),
                                          C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.sg_solver_set_profile.argtypes = [sp, C.c_int]
+    L.sg_solver_upload.argtypes = [sp, C.c_void_p, C.c_char_p, C.c_size_t]
+    L.sg_solver_download.argtypes = [sp, C.c_void_p, C.c_char_p, C.c_size_t]
+    L.sg_solver_initial.argtypes = [sp, C.c_void_p, C.c_char_p, C.c_size_t]
     L.sg_solver_destroy.argtypes = [sp]
     L.sg_solver_destroy.restype = None
     L.sg_plan_info.argtypes = [C.c_int, C.c_int, C.c_long, C.POINTER(C.c_long), C.c_char_p, C.c_size_t,

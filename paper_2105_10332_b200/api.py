@@ -342,6 +342,25 @@ class Solver:
         finally:
             self._L.sg_free_result(C.byref(res))
 
+    def upload(self, host) -> None:
+        """Replace level 0 from a host array [var][ny][nx] float64 (numpy, or a
+        pinned torch CPU tensor): the e2e input path."""
+        err = _c.errbuf()
+        p = host.data_ptr() if hasattr(host, "data_ptr") else host.ctypes.data
+        _check(self._L.sg_solver_upload(self._h, C.c_void_p(p), err, len(err)), err)
+
+    def download(self, host) -> None:
+        """Final field into a host array [var][ny][nx] float64."""
+        err = _c.errbuf()
+        p = host.data_ptr() if hasattr(host, "data_ptr") else host.ctypes.data
+        _check(self._L.sg_solver_download(self._h, C.c_void_p(p), err, len(err)), err)
+
+    def initial(self, host) -> None:
+        """The initial condition make_setup computed (engine.cpp:27-70) into a host array."""
+        err = _c.errbuf()
+        p = host.data_ptr() if hasattr(host, "data_ptr") else host.ctypes.data
+        _check(self._L.sg_solver_initial(self._h, C.c_void_p(p), err, len(err)), err)
+
     def kernel_stats(self) -> dict:
         s, n, b, u = C.c_double(), C.c_long(), C.c_double(), C.c_double()
         self._L.sg_solver_kernel_stats(self._h, 0, C.byref(s), C.byref(n), C.byref(b), C.byref(u))

@@ -119,6 +119,21 @@ int sg_solver_kernel_stats(sg_solver* s, int which, double* seconds, long* launc
     return SG_OK;
 }
 
+int sg_solver_upload(sg_solver* s, const double* host, char* err, size_t errlen) {
+    return guard(err, errlen, [&] { s->s->upload(host); });
+}
+
+int sg_solver_download(sg_solver* s, double* host, char* err, size_t errlen) {
+    return guard(err, errlen, [&] { s->s->download(host); });
+}
+
+int sg_solver_initial(sg_solver* s, double* host, char* err, size_t errlen) {
+    return guard(err, errlen, [&] {
+        const auto& v = s->s->setup().initial;
+        std::memcpy(host, v.data(), v.size() * sizeof(double));
+    });
+}
+
 int sg_solver_set_profile(sg_solver* s, int on) {
     s->s->profile = on != 0;
     return SG_OK;

@@ -190,10 +190,53 @@ void Solver::build_swept() {
             d.d_lev[kd] = dev_upload(d, lv);
             d.d_exp_off[kd] = dev_upload(d, K.exp_off);
             d.d_exp_vs[kd] = dev_upload(d, K.exp_vstride);
+            std::vector<int4> ln;
+            std::vector<int2> pt;
+            for (const auto& e : K.lanes) ln.push_back(make_int4(e[0], e[1], e[2], e[3]));
+            for (const auto& e : K.pitch) pt.push_back(make_int2(e[0], e[1]));
+            d.d_lanes[kd] = dev_upload(d, ln);
+            d.d_pitch[kd] = dev_upload(d, pt);
+            std::vector<DevCtaLevel> cl;
+            for (const auto& e : K.cta_levels) {
+                DevCtaLevel x{e[0], e[1], e[2], e[3], e[4], e[5], e[6], e[7], e[8], e[9],
+                              e[3] > 0 ? 1.0f / static_cast<float>(e[3]) : 0.0f, 0};
+                if (e[3] > 0 && e[4] == 0) fail(SG_EINVAL, "swept: phase rectangle wider than a CTA");
+                cl.push_back(x);
+            }
+            d.d_clev[kd] = dev_upload(d, cl);
+            std::vector<int2> el;
+            for (const auto& e : K.exp_lvl) el.push_back(make_int2(e[0], e[1]));
+            d.d_exp_lvl[kd] = dev_upload(d, el);
+            d.d_exp_begin[kd] = dev_upload(d, K.exp_begin);
+            std::vector<int4> tl;
+            for (const auto& e : K.tlanes) tl.push_back(make_int4(e[0], e[1], e[2], e[3]));
+            d.d_tlanes[kd] = dev_upload(d, tl);
+            std::vector<int4> cv;
+            int xb = 1 << 30;
+            for (int r = 1; r <= K.nlev; ++r) xb = std::min(xb, K.at(r).comp.x0);
+            for (int r = 1; r <= K.nlev; ++r) {
+                const PlanLevel& Lc = K.at(r);
+                const PlanLevel& Lp = K.at(r - 1);
+                cv.push_back(make_int4(Lc.comp.x0, Lc.comp.x1, Lc.comp.y0, Lc.comp.y1));
+                cv.push_back(make_int4(Lp.off - Lp.bbox.y0 * Lp.bbox.w() - Lp.bbox.x0, Lp.bbox.w(),
+                                       Lc.off - Lc.bbox.y0 * Lc.bbox.w() - Lc.bbox.x0, Lc.bbox.w()));
+            }
+            d.d_colv[kd] = dev_upload(d, cv);
+            d.xbase[kd] = K.nlev > 0 ? xb : 0;
         }
         for (const ClassTab& T : P.classes) {
             std::vector<int4> im, in;
-            for (const Import& x : T.imports) im.push_back(make_int4(x.seg, x.src, x.dst, x.vstride));
+            std::vector<int2> im2;
+            for (const Import& x : T.imports) {
+                if (x.src >= (1 << 20) || x.seg >= (1 << 11)) fail(SG_ELOGIC, "swept: import table overflow");
+                im.push_back(make_int4(x.seg, x.src, x.dst, x.vstride));
+                im2.push_back(make_int2((x.seg << 20) | x.src, x.dst));
+            }
+            d.d_imp2.push_back(dev_upload(d, im2));
+            std::vector<int2> cp;
+            for (const auto& e : T.copies) cp.push_back(make_int2(e[0], e[1]));
+            d.d_copies.push_back(dev_upload(d, cp));
+            d.d_copy_begin.push_back(dev_upload(d, T.copy_begin));
             for (const InitImport& x : T.inits) in.push_back(make_int4(x.rx, x.ry, x.dst, x.vstride));
             d.d_imp.push_back(dev_upload(d, im));
             d.d_init.push_back(dev_upload(d, in));
@@ -220,11 +263,41 @@ void Solver::build_swept() {
             a.rmin = K.rmin;
             a.smem_doubles = K.smem_doubles;
             a.nexp = static_cast<int>(K.exp_cells.size());
+            a.split = K.split;
+            a.nexp_early = K.nexp_early;
             a.epad = K.epad;
             a.lev = d.d_lev[L.kind];
             a.exp_off = d.d_exp_off[L.kind];
             a.exp_vs = d.d_exp_vs[L.kind];
+            a.lanes = d.d_lanes[L.kind];
+            a.pitch = d.d_pitch[L.kind];
+            a.clev = d.d_clev[L.kind];
+            a.tw = K.tw;
+            a.tx0 = K.tx0;
+            a.ty0 = K.ty0;
+            a.tile_doubles = K.tw * K.th;
+            a.npacked = static_cast<int>(T.imports.size() + T.inits.size());
+            a.warp_doubles = a.npacked + 2 * a.tile_doubles;
+            a.warp_doubles += a.warp_doubles & 1;  // 16-byte aligned per warp
+            a.copies = d.d_copies[L.cls];
+            a.copy_begin = d.d_copy_begin[L.cls];
+            a.exp_lvl = d.d_exp_lvl[L.kind];
+            a.exp_begin = d.d_exp_begin[L.kind];
+            a.tlanes = d.d_tlanes[L.kind];
+            a.colv = d.d_colv[L.kind];
+            a.xbase = d.xbase[L.kind];
+            {
+                int cols = 0;
+                for (int kd = 0; kd < K_NKINDS; ++kd)
+                    for (int r = 1; r <= P.kinds[kd].nlev; ++r)
+                        cols = std::max(cols, P.kinds[kd].at(r).comp.x1 - d.xbase[kd]);
+                a.lpi = 1;
+                while (a.lpi < cols) a.lpi <<= 1;
+                if (a.lpi > 32) fail(SG_EINVAL, "swept: block wider than a warp (b - 2n > 32)");
+                a.lpi = std::max(a.lpi, 8);  // <= 4 instances per warp
+            }
             a.imports = d.d_imp[L.cls];
+            a.imports2 = d.d_imp2[L.cls];
             a.nimp = static_cast<int>(T.imports.size());
             a.inits = d.d_init[L.cls];
             a.ninit = static_cast<int>(T.inits.size());
@@ -553,6 +626,74 @@ void Solver::fetch(sg_result* r) {
     r->cell_updates = cell_updates_;
     r->kernel_launches = launches_;
     r->final_field = field;
+}
+
+void Solver::upload(const double* host) {
+    // Level 0 from a host field [var][ny][nx] (pinned host memory is DMA'd directly).
+    const Equation& eq = setup_.eq;
+    const std::size_t nx = setup_.nx, ny = setup_.ny;
+    for (auto& pb : parts_) {
+        DeviceCtx& d = devs_[pb.dev];
+        cudaSetDevice(d.dev);
+        for (int v = 0; v < eq.nvars; ++v) {
+            const double* src = host + (v * ny + static_cast<std::size_t>(pb.pj) * ph_) * nx + pb.pi * pw_;
+            if (cfg_.engine == SG_SWEPT) {
+                ck(cudaMemcpy2DAsync(pb.init + static_cast<std::size_t>(v) * ph_ * pw_, pw_ * sizeof(double), src,
+                                     nx * sizeof(double), pw_ * sizeof(double), ph_, cudaMemcpyHostToDevice,
+                                     d.stream),
+                   "upload");
+            } else {
+                const int n = eq.halo, pitch = pw_ + 2 * n, rows = ph_ + 2 * n;
+                double* dst = pb.init_ghosted + static_cast<std::size_t>(v) * pitch * rows;
+                auto copy = [&](int gx0, int gy0, int w, int h, int lx, int ly) {
+                    // global window (wrapped start) -> local ghosted coords (lx, ly) in [-n, pw+n)
+                    const int sx = ((gx0 % (int)nx) + (int)nx) % (int)nx, sy = ((gy0 % (int)ny) + (int)ny) % (int)ny;
+                    ck(cudaMemcpy2DAsync(dst + static_cast<std::size_t>(ly + n) * pitch + (lx + n), pitch * sizeof(double),
+                                         host + (v * ny + sy) * nx + sx, nx * sizeof(double), w * sizeof(double), h,
+                                         cudaMemcpyHostToDevice, d.stream),
+                       "upload");
+                };
+                const int gx = pb.pi * pw_, gy = pb.pj * ph_;
+                copy(gx, gy, pw_, ph_, 0, 0);
+                copy(gx - n, gy, n, ph_, -n, 0);
+                copy(gx + pw_, gy, n, ph_, pw_, 0);
+                copy(gx, gy - n, pw_, n, 0, -n);
+                copy(gx, gy + ph_, pw_, n, 0, ph_);
+            }
+        }
+    }
+    for (auto& d : devs_) {
+        cudaSetDevice(d.dev);
+        ck(cudaStreamSynchronize(d.stream), "upload sync");
+    }
+}
+
+void Solver::download(double* host) {
+    const Equation& eq = setup_.eq;
+    const std::size_t nx = setup_.nx, ny = setup_.ny;
+    for (auto& pb : parts_) {
+        DeviceCtx& d = devs_[pb.dev];
+        cudaSetDevice(d.dev);
+        for (int v = 0; v < eq.nvars; ++v) {
+            double* dst = host + (v * ny + static_cast<std::size_t>(pb.pj) * ph_) * nx + pb.pi * pw_;
+            if (cfg_.engine == SG_SWEPT) {
+                ck(cudaMemcpy2DAsync(dst, nx * sizeof(double), pb.out + static_cast<std::size_t>(v) * ph_ * pw_,
+                                     pw_ * sizeof(double), pw_ * sizeof(double), ph_, cudaMemcpyDeviceToHost, d.stream),
+                   "download");
+            } else {
+                const int n = eq.halo, pitch = pw_ + 2 * n, rows = ph_ + 2 * n;
+                const double* src = pb.ring[final_level_ % (eq.substeps + 1)] +
+                                    static_cast<std::size_t>(v) * pitch * rows + static_cast<std::size_t>(n) * pitch + n;
+                ck(cudaMemcpy2DAsync(dst, nx * sizeof(double), src, pitch * sizeof(double), pw_ * sizeof(double), ph_,
+                                     cudaMemcpyDeviceToHost, d.stream),
+                   "download");
+            }
+        }
+    }
+    for (auto& d : devs_) {
+        cudaSetDevice(d.dev);
+        ck(cudaStreamSynchronize(d.stream), "download sync");
+    }
 }
 
 void Solver::kernel_stats(int which, double* seconds, long* launches, double* alg_bytes, double* updates) const {

@@ -36,7 +36,18 @@ struct DeviceCtx {
     DevLevel* d_lev[K_NKINDS] = {};
     int* d_exp_off[K_NKINDS] = {};
     int* d_exp_vs[K_NKINDS] = {};
+    int4* d_lanes[K_NKINDS] = {};
+    int2* d_pitch[K_NKINDS] = {};
+    DevCtaLevel* d_clev[K_NKINDS] = {};
+    int2* d_exp_lvl[K_NKINDS] = {};
+    int* d_exp_begin[K_NKINDS] = {};
+    int4* d_tlanes[K_NKINDS] = {};
+    int4* d_colv[K_NKINDS] = {};
+    int xbase[K_NKINDS] = {};
+    std::vector<int2*> d_copies;
+    std::vector<int*> d_copy_begin;
     std::vector<int4*> d_imp, d_init;
+    std::vector<int2*> d_imp2;
     double** d_rec_tab = nullptr;
     const double** d_init_tab = nullptr;
     double** d_out_tab = nullptr;
@@ -54,6 +65,8 @@ class Solver {
     void reset();
     double solve();  // device seconds (max over devices)
     void fetch(sg_result* r);
+    void upload(const double* host);    // replace level 0 from a host field
+    void download(double* host);        // final field into a host buffer
     void kernel_stats(int which, double* seconds, long* launches, double* alg_bytes, double* updates) const;
 
     const Setup& setup() const { return setup_; }

@@ -164,6 +164,195 @@ __global__ void __launch_bounds__(128) swept_phase_kernel(const __grid_constant_
     if (err) *A.err = 1;
 }
 
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// Heat phase kernel: one WARP per block instance, WPC instances per CTA, no
+// CTA-wide barriers (the warp is the instance's only owner).
+//  1. gather: cp.async lands every imported edge cell (a record entry of an
+//     earlier phase) at its final place in the instance's level storage;
+//  2. levels 1..nlev on chip: lane l takes the (column, row-chunk) item the
+//     plan's lane map gives it and walks down the chunk, four rows per trip,
+//     centre/south kept in registers (3 LDS + 1 STS per update);
+//  3. scatter: the record entries (cells later phases read) go to HBM in
+//     record order, plus ghost copies from partition-edge instances.  Levels
+//     above `split` (an Octahedron's shrinking half, which gets no imports)
+//     reuse the storage of the dead lower levels, so the lower levels'
+//     exports are flushed first.
+template <int WPC>
+__global__ void __launch_bounds__(WPC * 32) swept_heat_kernel(const __grid_constant__ SweptArgs A) {
+    extern __shared__ double sm[];
+    __shared__ const double* segbase[WPC][kMaxSegs];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ninst = A.pbx * A.pby;
+    const int inst = blockIdx.x * WPC + warp;
+    if (inst >= ninst) return;
+    const int part = A.dev_parts[blockIdx.y];
+    const int pi = part % A.px, pj = part / A.px;
+    const int bi = inst % A.pbx, bj = inst / A.pbx;
+    const int half = A.frame * (A.b / 2);
+    double* S = sm + warp * A.smem_doubles;
+    const double** sb = segbase[warp];
+
+    // ---- 1. gather
+    if (lane < A.nsegs) {
+        const DevSeg sg = A.segs[lane];
+        const long ext = (long)(bj + sg.dj + A.ghost) * A.extw + (bi + sg.di + A.ghost);
+        sb[lane] = A.rec[part * A.nslots + sg.slot] + ext * sg.epad;
+    }
+    __syncwarp();
+    {
+        const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(S));
+        int i = lane;
+        for (; i + 96 < A.nimp; i += 128) {
+            const int2 e0 = __ldg(&A.imports2[i]), e1 = __ldg(&A.imports2[i + 32]);
+            const int2 e2 = __ldg(&A.imports2[i + 64]), e3 = __ldg(&A.imports2[i + 96]);
+            const double* g0 = sb[e0.x >> 20] + (e0.x & 0xFFFFF);
+            const double* g1 = sb[e1.x >> 20] + (e1.x & 0xFFFFF);
+            const double* g2 = sb[e2.x >> 20] + (e2.x & 0xFFFFF);
+            const double* g3 = sb[e3.x >> 20] + (e3.x & 0xFFFFF);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sbase + 8u * e0.y), "l"(g0) : "memory");
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sbase + 8u * e1.y), "l"(g1) : "memory");
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sbase + 8u * e2.y), "l"(g2) : "memory");
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sbase + 8u * e3.y), "l"(g3) : "memory");
+        }
+        for (; i < A.nimp; i += 32) {
+            const int2 e = __ldg(&A.imports2[i]);
+            const double* g = sb[e.x >> 20] + (e.x & 0xFFFFF);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sbase + 8u * e.y), "l"(g) : "memory");
+        }
+    }
+    for (int i = lane; i < A.ninit; i += 32) {
+        const int4 im = __ldg(&A.inits[i]);
+        const int gx = wrapi(pi * A.pw + bi * A.b - half + im.x, A.nx);
+        const int gy = wrapi(pj * A.ph + bj * A.b - half + im.y, A.ny);
+        const int opi = gx / A.pw, opj = gy / A.ph;
+        S[im.z] = A.init_planes[opj * A.px + opi][(long)(gy - opj * A.ph) * A.pw + (gx - opi * A.pw)];
+    }
+    cp_async_wait_all();
+    __syncwarp();
+
+    const int gh = A.ghost;
+    double* dst = A.rec[part * A.nslots + A.my_slot] + ((long)(bj + gh) * A.extw + (bi + gh)) * A.epad;
+    const bool edge = bi < gh || bi >= A.pbx - gh || bj < gh || bj >= A.pby - gh;
+    auto flush = [&](int e0, int e1) {  // record entries [e0, e1) -> HBM (+ ghosts)
+        int e = e0 + lane;
+        for (; e + 96 < e1; e += 128) {
+            const int o0 = __ldg(&A.exp_off[e]), o1 = __ldg(&A.exp_off[e + 32]);
+            const int o2 = __ldg(&A.exp_off[e + 64]), o3 = __ldg(&A.exp_off[e + 96]);
+            const double v0 = S[o0], v1 = S[o1], v2 = S[o2], v3 = S[o3];
+            dst[e] = v0;
+            dst[e + 32] = v1;
+            dst[e + 64] = v2;
+            dst[e + 96] = v3;
+        }
+        for (; e < e1; e += 32) dst[e] = S[__ldg(&A.exp_off[e])];
+        if (edge)
+            for (int e2 = e0 + lane; e2 < e1; e2 += 32) {
+                const double v = S[__ldg(&A.exp_off[e2])];
+                for (int ej = -1; ej <= 1; ++ej)
+                    for (int ei = -1; ei <= 1; ++ei) {
+                        if (ei == 0 && ej == 0) continue;
+                        const int tbi = bi - ei * A.pbx, tbj = bj - ej * A.pby;
+                        if (tbi < -gh || tbi >= A.pbx + gh || tbj < -gh || tbj >= A.pby + gh) continue;
+                        const int tp = wrapi(pj + ej, A.py) * A.px + wrapi(pi + ei, A.px);
+                        A.rec[tp * A.nslots + A.my_slot][((long)(tbj + gh) * A.extw + (tbi + gh)) * A.epad + e2] = v;
+                    }
+            }
+    };
+
+    // ---- 2. levels
+    const double fx = A.c0, fy = A.c1;
+    for (int r = 1; r <= A.nlev; ++r) {
+        const int4 t = __ldg(&A.lanes[(r - 1) * 32 + lane]);
+        const int2 pt = __ldg(&A.pitch[r - 1]);
+        const int bp = pt.x, bc = pt.y;
+        const double* P = S + t.x;
+        double* D = S + t.y;
+        int n = t.z;
+        if (n > 0) {
+            double south = P[-bp], c = P[0];
+            for (; n >= 4; n -= 4) {
+                const double n1 = P[bp], n2 = P[2 * bp], n3 = P[3 * bp], n4 = P[4 * bp];
+                const double v1 = heat_update(c, P[1], P[-1], n1, south, fx, fy);
+                const double v2 = heat_update(n1, P[bp + 1], P[bp - 1], n2, c, fx, fy);
+                const double v3 = heat_update(n2, P[2 * bp + 1], P[2 * bp - 1], n3, n1, fx, fy);
+                const double v4 = heat_update(n3, P[3 * bp + 1], P[3 * bp - 1], n4, n2, fx, fy);
+                D[0] = v1;
+                D[bc] = v2;
+                D[2 * bc] = v3;
+                D[3 * bc] = v4;
+                south = n3;
+                c = n4;
+                P += 4 * bp;
+                D += 4 * bc;
+            }
+            for (; n > 0; --n) {
+                const double nn = P[bp];
+                D[0] = heat_update(c, P[1], P[-1], nn, south, fx, fy);
+                south = c;
+                c = nn;
+                P += bp;
+                D += bc;
+            }
+        }
+        if (r == A.r_out && t.z > 0) {
+            const int x = t.w & 0xFFFF, y0 = t.w >> 16;
+            const double* Dv = S + t.y;
+            for (int y = y0; y < y0 + t.z; ++y, Dv += bc) {
+                const int gx = wrapi(pi * A.pw + bi * A.b - half + x, A.nx);
+                const int gy = wrapi(pj * A.ph + bj * A.b - half + y, A.ny);
+                const int opi = gx / A.pw, opj = gy / A.ph;
+                A.out_planes[opj * A.px + opi][(long)(gy - opj * A.ph) * A.pw + (gx - opi * A.pw)] = *Dv;
+            }
+        }
+        __syncwarp();
+        if (r == A.split && A.nexp_early > 0) {
+            flush(0, A.nexp_early);
+            __syncwarp();
+        }
+    }
+    // ---- 3. scatter the rest of the record
+    if (A.nexp > A.nexp_early) flush(A.nexp_early, A.nexp);
+}
+
+// Standard heat step, column marching: a thread owns one column of a
+// 128 x ROWS tile and walks down it keeping centre/south in registers, so each
+// plane value is read from HBM once (E/W come from the neighbouring lanes'
+// loads through L1).  Partition-edge cells are pushed into the neighbours'
+// ghost frames (same kernel: the "fused halo export").
+template <int ROWS>
+__global__ void __launch_bounds__(128) std_heat_kernel(const __grid_constant__ StdArgs A) {
+    const int x = blockIdx.x * 128 + threadIdx.x;
+    const int ybeg = blockIdx.y * ROWS;
+    if (x >= A.pw) return;
+    const int part = A.dev_parts[blockIdx.z];
+    const int P = A.pitch;
+    const int yend = min(ybeg + ROWS, A.ph);
+    const double* r = A.read1[part] + (long)(ybeg + 1) * P + (x + 1);
+    double* o = A.out[part] + (long)(ybeg + 1) * P + (x + 1);
+    const int pi = part % A.px, pj = part / A.px;
+    double* left = (x == 0) ? A.out[pj * A.px + (pi + A.px - 1) % A.px] : nullptr;
+    double* right = (x == A.pw - 1) ? A.out[pj * A.px + (pi + 1) % A.px] : nullptr;
+    double south = __ldg(r - P), c = __ldg(r);
+    for (int y = ybeg; y < yend; ++y) {
+        const double north = __ldg(r + P);
+        const double v = heat_update(c, __ldg(r + 1), __ldg(r - 1), north, south, A.c0, A.c1);
+        *o = v;
+        if (left) left[(long)(y + 1) * P + (A.pw + 1)] = v;
+        if (right) right[(long)(y + 1) * P] = v;
+        if (y == 0) A.out[((pj + A.py - 1) % A.py) * A.px + pi][(long)(A.ph + 1) * P + (x + 1)] = v;
+        if (y == A.ph - 1) A.out[((pj + 1) % A.py) * A.px + pi][(x + 1)] = v;
+        south = c;
+        c = north;
+        r += P;
+        o += P;
+    }
+}
+
 template <int PROB>
 __global__ void __launch_bounds__(256) std_step_kernel(const __grid_constant__ StdArgs A) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
@@ -247,6 +436,19 @@ __global__ void substep_rects_kernel(int stage, const double* __restrict__ r1, c
 
 cudaError_t launch_swept(int problem, const SweptArgs& a, int G, int threads, cudaStream_t s) {
     const int ninst = a.pbx * a.pby;
+    if (problem == 0) {
+        const size_t per_inst = static_cast<size_t>(a.smem_doubles) * sizeof(double);
+        auto go = [&](auto kern, int wpc) {
+            const size_t smem = wpc * per_inst;
+            if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            dim3 grid((ninst + wpc - 1) / wpc, a.ndev_parts);
+            kern<<<grid, wpc * 32, smem, s>>>(a);
+            return cudaGetLastError();
+        };
+        if (4 * per_inst <= 64 * 1024) return go(swept_heat_kernel<4>, 4);
+        if (2 * per_inst <= 100 * 1024) return go(swept_heat_kernel<2>, 2);
+        return go(swept_heat_kernel<1>, 1);
+    }
     const int grid = a.ndev_parts * ((ninst + G - 1) / G);
     const size_t smem = static_cast<size_t>(G) * a.smem_doubles * sizeof(double);
     if (problem == 0) {
@@ -262,6 +464,12 @@ cudaError_t launch_swept(int problem, const SweptArgs& a, int G, int threads, cu
 }
 
 cudaError_t launch_std(int problem, const StdArgs& a, cudaStream_t s) {
+    if (problem == 0) {
+        constexpr int ROWS = 32;
+        dim3 grid((a.pw + 127) / 128, (a.ph + ROWS - 1) / ROWS, a.ndev_parts);
+        std_heat_kernel<ROWS><<<grid, 128, 0, s>>>(a);
+        return cudaGetLastError();
+    }
     dim3 block(32, 8);
     dim3 grid((a.pw + 31) / 32, (a.ph + 7) / 8, a.ndev_parts);
     if (problem == 0) std_step_kernel<0><<<grid, block, 0, s>>>(a);
