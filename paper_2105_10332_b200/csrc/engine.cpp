@@ -264,6 +264,17 @@ void Solver::build_swept() {
             a.smem_doubles = K.smem_doubles;
             a.nexp = static_cast<int>(K.exp_cells.size());
             a.split = K.split;
+            {
+                int ps = 0, fx = 0;
+                for (int kd = 0; kd < K_NKINDS; ++kd)
+                    for (int r = 1; r <= P.kinds[kd].nlev; ++r) {
+                        const Rect c = P.kinds[kd].at(r).comp;
+                        ps = std::max(ps, (c.w() + 4) * (c.h() + 4));
+                        fx = std::max(fx, 4 * std::max(c.h() * (c.w() + 1), (c.h() + 1) * c.w()));
+                    }
+                a.ps_doubles = (ps + 1) & ~1;
+                a.fx_doubles = (fx + 1) & ~1;
+            }
             a.nexp_early = K.nexp_early;
             a.epad = K.epad;
             a.lev = d.d_lev[L.kind];

@@ -319,14 +319,184 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_kernel(const __grid_const
     if (A.nexp > A.nexp_early) flush(A.nexp_early, A.nexp);
 }
 
-// Standard heat step, column marching: a thread owns one column of a
-// 128 x ROWS tile and walks down it keeping centre/south in registers, so each
-// plane value is read from HBM once (E/W come from the neighbouring lanes'
-// loads through L1).  Partition-edge cells are pushed into the neighbours'
-// ghost frames (same kernel: the "fused halo export").
+// Euler phase kernel: one CTA (128 threads) per block instance.  Gather as
+// the heat kernel (4 variables per record entry), then every level of the
+// phase runs through euler_rect on shared memory (pressures, shared x/y
+// interface fluxes, update), then the record is scattered.
+__global__ void __launch_bounds__(128) swept_euler_kernel(const __grid_constant__ SweptArgs A) {
+    extern __shared__ double S[];
+    __shared__ const double* sb[kMaxSegs];
+    const int tid = threadIdx.x, T = 128;
+    const int inst = blockIdx.x;
+    const int part = A.dev_parts[blockIdx.y];
+    const int pi = part % A.px, pj = part / A.px;
+    const int bi = inst % A.pbx, bj = inst / A.pbx;
+    const int half = A.frame * (A.b / 2);
+    double* ps = S + A.smem_doubles;
+    double* fxs = ps + A.ps_doubles;
+    double* fys = fxs + A.fx_doubles;
+    int err = 0;
+
+    if (tid < A.nsegs) {
+        const DevSeg sg = A.segs[tid];
+        const long ext = (long)(bj + sg.dj + A.ghost) * A.extw + (bi + sg.di + A.ghost);
+        sb[tid] = A.rec[part * A.nslots + sg.slot] + ext * 4 * sg.epad;
+    }
+    __syncthreads();
+    {
+        const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(S));
+        for (int i = tid; i < A.nimp; i += T) {
+            const int4 e = __ldg(&A.imports[i]);
+            const int ep = A.segs[e.x].epad;
+            const double* g = sb[e.x] + e.y;
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sbase + 8u * (e.z + v * e.w)),
+                             "l"(g + v * ep)
+                             : "memory");
+        }
+    }
+    for (int i = tid; i < A.ninit; i += T) {
+        const int4 im = __ldg(&A.inits[i]);
+        const int gx = wrapi(pi * A.pw + bi * A.b - half + im.x, A.nx);
+        const int gy = wrapi(pj * A.ph + bj * A.b - half + im.y, A.ny);
+        const int opi = gx / A.pw, opj = gy / A.ph;
+        const double* src = A.init_planes[opj * A.px + opi] + (long)(gy - opj * A.ph) * A.pw + (gx - opi * A.pw);
+        const long pl = (long)A.pw * A.ph;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) S[im.z + v * im.w] = src[v * pl];
+    }
+    cp_async_wait_all();
+    __syncthreads();
+
+    const int gh = A.ghost;
+    double* dst = A.rec[part * A.nslots + A.my_slot] + ((long)(bj + gh) * A.extw + (bi + gh)) * 4 * A.epad;
+    const bool edge = bi < gh || bi >= A.pbx - gh || bj < gh || bj >= A.pby - gh;
+    auto flush = [&](int e0, int e1) {
+        for (int e = e0 + tid; e < e1; e += T) {
+            const int so = __ldg(&A.exp_off[e]), vs = __ldg(&A.exp_vs[e]);
+            double val[4];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) val[v] = S[so + v * vs];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) dst[v * A.epad + e] = val[v];
+            if (edge)
+                for (int ej = -1; ej <= 1; ++ej)
+                    for (int ei = -1; ei <= 1; ++ei) {
+                        if (ei == 0 && ej == 0) continue;
+                        const int tbi = bi - ei * A.pbx, tbj = bj - ej * A.pby;
+                        if (tbi < -gh || tbi >= A.pbx + gh || tbj < -gh || tbj >= A.pby + gh) continue;
+                        const int tp = wrapi(pj + ej, A.py) * A.px + wrapi(pi + ei, A.px);
+                        double* d = A.rec[tp * A.nslots + A.my_slot] + ((long)(tbj + gh) * A.extw + (tbi + gh)) * 4 * A.epad + e;
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) d[v * A.epad] = val[v];
+                    }
+        }
+    };
+
+    for (int r = 1; r <= A.nlev; ++r) {
+        const int stage = (A.stage0 + r - 1) & 1;
+        const DevLevel Lc = A.lev[r - A.rmin];
+        const DevLevel Lp = A.lev[r - 1 - A.rmin];
+        const DevLevel Lb = stage == 1 ? A.lev[r - 2 - A.rmin] : Lp;
+        auto Q = [&](int x, int y, int v) { return S[Lp.off + v * Lp.vstride + (y - Lp.by0) * Lp.bw + (x - Lp.bx0)]; };
+        auto B = [&](int x, int y, int v) { return S[Lb.off + v * Lb.vstride + (y - Lb.by0) * Lb.bw + (x - Lb.bx0)]; };
+        const bool out = r == A.r_out;
+        auto O = [&](int x, int y, const double o[4]) {
+            double* d = S + Lc.off + (y - Lc.by0) * Lc.bw + (x - Lc.bx0);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) d[v * Lc.vstride] = o[v];
+            if (out) {
+                const int gx = wrapi(pi * A.pw + bi * A.b - half + x, A.nx);
+                const int gy = wrapi(pj * A.ph + bj * A.b - half + y, A.ny);
+                const int opi = gx / A.pw, opj = gy / A.ph;
+                double* g = A.out_planes[opj * A.px + opi] + (long)(gy - opj * A.ph) * A.pw + (gx - opi * A.pw);
+                const long pl = (long)A.pw * A.ph;
+#pragma unroll
+                for (int v = 0; v < 4; ++v) g[v * pl] = o[v];
+            }
+        };
+        euler_rect(tid, T, Lc.cx0, Lc.cx1, Lc.cy0, Lc.cy1, Q, B, O, ps, fxs, fys, A.c0, stage == 0 ? A.c1 : A.c3,
+                   stage == 0 ? A.c2 : A.c4, err);
+        if (r == A.split && A.nexp_early > 0) {
+            flush(0, A.nexp_early);
+            __syncthreads();
+        }
+    }
+    if (A.nexp > A.nexp_early) flush(A.nexp_early, A.nexp);
+    if (err) *A.err = 1;
+}
+
+// Standard Euler step on a TX x TY output tile per CTA: the cross-shaped
+// radius-2 neighbourhood of the tile is staged in shared memory, then
+// euler_rect (shared interface fluxes); boundary cells are pushed into the
+// neighbouring partitions' ghost frames.
+template <int TX, int TY>
+__global__ void __launch_bounds__(256) std_euler_kernel(const __grid_constant__ StdArgs A) {
+    constexpr int QW = TX + 4, QH = TY + 4;
+    __shared__ double q[4][QH][QW];
+    __shared__ double ps[QH * QW];
+    __shared__ double fxs[4 * TY * (TX + 1)];
+    __shared__ double fys[4 * (TY + 1) * TX];
+    const int tid = threadIdx.x, T = 256;
+    const int part = A.dev_parts[blockIdx.z];
+    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+    const int x1 = min(x0 + TX, A.pw), y1 = min(y0 + TY, A.ph);
+    const int P = A.pitch;
+    const long pl = (long)A.pitch * A.rows;
+    const double* r1 = A.read1[part];
+    // stage the tile + radius-2 frame (corners included; they are never used)
+    for (int i = tid; i < QW * QH; i += T) {
+        const int yy = i / QW, xx = i - yy * QW;
+        const int x = x0 - 2 + xx, y = y0 - 2 + yy;
+        if (x < -2 || x >= A.pw + 2 || y < -2 || y >= A.ph + 2) continue;
+        const double* g = r1 + (long)(y + 2) * P + (x + 2);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) q[v][yy][xx] = __ldg(g + v * pl);
+    }
+    __syncthreads();
+    const int pi = part % A.px, pj = part / A.px;
+    const double* r2 = A.read2[part];
+    const bool corr = A.stage == 1;
+    auto Q = [&](int x, int y, int v) { return q[v][y - y0 + 2][x - x0 + 2]; };
+    auto B = [&](int x, int y, int v) {
+        return corr ? __ldg(r2 + v * pl + (long)(y + 2) * P + (x + 2)) : q[v][y - y0 + 2][x - x0 + 2];
+    };
+    auto O = [&](int x, int y, const double o[4]) {
+        const long idx = (long)(y + 2) * P + (x + 2);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) A.out[part][idx + v * pl] = o[v];
+        if (x < 2) {
+            double* g = A.out[pj * A.px + (pi + A.px - 1) % A.px] + (long)(y + 2) * P + (x + A.pw + 2);
+            for (int v = 0; v < 4; ++v) g[v * pl] = o[v];
+        }
+        if (x >= A.pw - 2) {
+            double* g = A.out[pj * A.px + (pi + 1) % A.px] + (long)(y + 2) * P + (x - A.pw + 2);
+            for (int v = 0; v < 4; ++v) g[v * pl] = o[v];
+        }
+        if (y < 2) {
+            double* g = A.out[((pj + A.py - 1) % A.py) * A.px + pi] + (long)(y + A.ph + 2) * P + (x + 2);
+            for (int v = 0; v < 4; ++v) g[v * pl] = o[v];
+        }
+        if (y >= A.ph - 2) {
+            double* g = A.out[((pj + 1) % A.py) * A.px + pi] + (long)(y - A.ph + 2) * P + (x + 2);
+            for (int v = 0; v < 4; ++v) g[v * pl] = o[v];
+        }
+    };
+    int err = 0;
+    euler_rect(tid, T, x0, x1, y0, y1, Q, B, O, ps, fxs, fys, A.c0, A.c1, A.c2, err);
+    if (err) *A.err = 1;
+}
+
+// Standard heat step, column marching: a thread owns two adjacent columns of
+// a 256 x ROWS tile and walks down them four rows per trip with 16-byte
+// loads/stores; centre/south stay in registers and the E/W neighbours of the
+// pair come from the L1-resident neighbouring pairs, so each plane value
+// crosses HBM once.  Partition-edge cells are pushed into the neighbours'
+// ghost frames by the same kernel (the fused halo export).  Requires pw even.
 template <int ROWS>
 __global__ void __launch_bounds__(128) std_heat_kernel(const __grid_constant__ StdArgs A) {
-    const int x = blockIdx.x * 128 + threadIdx.x;
+    const int x = 2 * (blockIdx.x * 128 + threadIdx.x);
     const int ybeg = blockIdx.y * ROWS;
     if (x >= A.pw) return;
     const int part = A.dev_parts[blockIdx.z];
@@ -335,19 +505,47 @@ __global__ void __launch_bounds__(128) std_heat_kernel(const __grid_constant__ S
     const double* r = A.read1[part] + (long)(ybeg + 1) * P + (x + 1);
     double* o = A.out[part] + (long)(ybeg + 1) * P + (x + 1);
     const int pi = part % A.px, pj = part / A.px;
-    double* left = (x == 0) ? A.out[pj * A.px + (pi + A.px - 1) % A.px] : nullptr;
-    double* right = (x == A.pw - 1) ? A.out[pj * A.px + (pi + 1) % A.px] : nullptr;
-    double south = __ldg(r - P), c = __ldg(r);
-    for (int y = ybeg; y < yend; ++y) {
-        const double north = __ldg(r + P);
-        const double v = heat_update(c, __ldg(r + 1), __ldg(r - 1), north, south, A.c0, A.c1);
-        *o = v;
-        if (left) left[(long)(y + 1) * P + (A.pw + 1)] = v;
-        if (right) right[(long)(y + 1) * P] = v;
-        if (y == 0) A.out[((pj + A.py - 1) % A.py) * A.px + pi][(long)(A.ph + 1) * P + (x + 1)] = v;
-        if (y == A.ph - 1) A.out[((pj + 1) % A.py) * A.px + pi][(x + 1)] = v;
+    const double fx = A.c0, fy = A.c1;
+    // ghost frame pitch is pw + 2 (odd offset +1): rows are 8-byte aligned only,
+    // so the pair is loaded as two 8-byte loads the compiler merges where legal
+    auto ld2 = [](const double* p) { return make_double2(__ldg(p), __ldg(p + 1)); };
+    double2 south = ld2(r - P), c = ld2(r);
+    int y = ybeg;
+    auto row = [&](double2 cc, double2 nn, double2 ss, const double* rr, double* oo, int yy) {
+        const double w = __ldg(rr - 1), e = __ldg(rr + 2);
+        const double v0 = heat_update(cc.x, cc.y, w, nn.x, ss.x, fx, fy);
+        const double v1 = heat_update(cc.y, e, cc.x, nn.y, ss.y, fx, fy);
+        oo[0] = v0;
+        oo[1] = v1;
+        if (x == 0) A.out[pj * A.px + (pi + A.px - 1) % A.px][(long)(yy + 1) * P + (A.pw + 1)] = v0;
+        if (x + 2 == A.pw) A.out[pj * A.px + (pi + 1) % A.px][(long)(yy + 1) * P] = v1;
+        if (yy == 0) {
+            double* g = A.out[((pj + A.py - 1) % A.py) * A.px + pi] + (long)(A.ph + 1) * P + (x + 1);
+            g[0] = v0;
+            g[1] = v1;
+        }
+        if (yy == A.ph - 1) {
+            double* g = A.out[((pj + 1) % A.py) * A.px + pi] + (x + 1);
+            g[0] = v0;
+            g[1] = v1;
+        }
+    };
+    for (; y + 4 <= yend; y += 4) {
+        const double2 n1 = ld2(r + P), n2 = ld2(r + 2 * P), n3 = ld2(r + 3 * P), n4 = ld2(r + 4 * P);
+        row(c, n1, south, r, o, y);
+        row(n1, n2, c, r + P, o + P, y + 1);
+        row(n2, n3, n1, r + 2 * P, o + 2 * P, y + 2);
+        row(n3, n4, n2, r + 3 * P, o + 3 * P, y + 3);
+        south = n3;
+        c = n4;
+        r += 4 * P;
+        o += 4 * P;
+    }
+    for (; y < yend; ++y) {
+        const double2 nn = ld2(r + P);
+        row(c, nn, south, r, o, y);
         south = c;
-        c = north;
+        c = nn;
         r += P;
         o += P;
     }
@@ -449,6 +647,14 @@ cudaError_t launch_swept(int problem, const SweptArgs& a, int G, int threads, cu
         if (2 * per_inst <= 100 * 1024) return go(swept_heat_kernel<2>, 2);
         return go(swept_heat_kernel<1>, 1);
     }
+    {
+        const size_t smem = static_cast<size_t>(a.smem_doubles + a.ps_doubles + 2 * a.fx_doubles) * sizeof(double);
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(swept_euler_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        dim3 grid(ninst, a.ndev_parts);
+        swept_euler_kernel<<<grid, 128, smem, s>>>(a);
+        return cudaGetLastError();
+    }
     const int grid = a.ndev_parts * ((ninst + G - 1) / G);
     const size_t smem = static_cast<size_t>(G) * a.smem_doubles * sizeof(double);
     if (problem == 0) {
@@ -464,10 +670,16 @@ cudaError_t launch_swept(int problem, const SweptArgs& a, int G, int threads, cu
 }
 
 cudaError_t launch_std(int problem, const StdArgs& a, cudaStream_t s) {
-    if (problem == 0) {
+    if (problem == 0 && a.pw % 2 == 0) {
         constexpr int ROWS = 32;
-        dim3 grid((a.pw + 127) / 128, (a.ph + ROWS - 1) / ROWS, a.ndev_parts);
+        dim3 grid((a.pw / 2 + 127) / 128, (a.ph + ROWS - 1) / ROWS, a.ndev_parts);
         std_heat_kernel<ROWS><<<grid, 128, 0, s>>>(a);
+        return cudaGetLastError();
+    }
+    if (problem == 1) {
+        constexpr int TX = 32, TY = 8;
+        dim3 grid((a.pw + TX - 1) / TX, (a.ph + TY - 1) / TY, a.ndev_parts);
+        std_euler_kernel<TX, TY><<<grid, 256, 0, s>>>(a);
         return cudaGetLastError();
     }
     dim3 block(32, 8);

@@ -33,6 +33,7 @@ struct SweptArgs {
     // kind layout
     int nlev, rmin, smem_doubles, nexp, epad;
     int split, nexp_early;   // flush exports [0, nexp_early) after level `split`
+    int ps_doubles, fx_doubles;  // euler scratch (pressure plane, per-axis flux arrays)
     const DevLevel* lev;     // [nlev - rmin + 1]
     const int* exp_off;      // [nexp]
     const int* exp_vs;       // [nexp]
