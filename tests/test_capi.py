@@ -1,0 +1,93 @@
+"""The C-ABI boundary without a GPU: the library loads, exports every entry
+point include/sweptgpu.h declares, validates configs like
+SolverConfig::validate (proj/src/config.cpp:31-62) and round-trips the
+reference JSON formats (config.cpp:79-125, engine.cpp:461-491)."""
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def test_library_exports_every_declared_symbol(sg):
+    from paper_2105_10332_b200 import _capi
+    lib = _capi.load()
+    hdr = (ROOT / "include" / "sweptgpu.h").read_text()
+    declared = set(re.findall(r"\b(sg_[a-z_]+)\s*\(", hdr))
+    assert declared, "header parse failed"
+    for name in sorted(declared):
+        assert hasattr(lib, name), f"{name} declared in sweptgpu.h but not exported"
+    assert declared == set(_capi.EXPORTS)
+
+
+def test_library_is_sm100a_and_fmad_free():
+    """The shipped cubin targets sm_100a only."""
+    import shutil
+    import subprocess
+    so = ROOT / "paper_2105_10332_b200" / "libsweptgpu.so"
+    if not shutil.which("cuobjdump"):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run(["cuobjdump", "--list-elf", str(so)], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["cuobjdump", "-sass", str(so)], capture_output=True, text=True).stdout
+    # -fmad=false: the stencil arithmetic never contracts (DFMA only inside IEEE div/sqrt sequences)
+    heat = sass.split("swept_heat_kernel")[1].split("Function :")[0] if "swept_heat_kernel" in sass else ""
+    assert heat and "DFMA" not in heat
+
+
+def test_no_cpu_fallback_without_gpu(sg):
+    if sg.device_count() >= 1:
+        pytest.skip("GPU present")
+    with pytest.raises(sg.CudaError):
+        sg.run(sg.SolverConfig(problem="heat", nx=32, block=8, steps=3))
+
+
+@pytest.mark.parametrize("kw", [
+    dict(nx=100, block=16),                 # nx not a block multiple (test_engine.cpp:129)
+    dict(nx=32, block=8, ranks=3),          # 4 columns over 3 ranks (:130-132)
+    dict(nx=32, block=8, heat_fourier=0.3), # unstable (:133-135)
+    dict(nx=32, block=8, share=1.5),        # (:136-138)
+    dict(nx=32, block=10),                  # b % 2n
+    dict(nx=32, block=8, steps=0),
+    dict(nx=32, block=8, mode="virtual"),   # simulated network: out of scope
+    dict(nx=64, block=8, ranks=4, px=2, py=3),
+])
+def test_validation_rejects(sg, kw):
+    with pytest.raises(sg.InvalidArgument):
+        sg.SolverConfig(**kw).validate()
+
+
+def test_validation_accepts(sg):
+    sg.SolverConfig(problem="euler", nx=96, block=16, steps=10, ranks=2).validate()
+    sg.SolverConfig(problem="heat", nx=64, ny=128, block=16, ranks=4, px=2, py=2).validate()
+
+
+def test_config_json_round_trip(sg):
+    j = {"problem": "euler", "nx": 96, "block": 16, "steps": 50, "ranks": 2, "engine": "standard",
+         "mode": "wall", "latency": 0.0, "pool_a": {"workers": 4, "cost": 1.0}, "pool_b": {"workers": 1, "cost": 3.0},
+         "cell_cost": 5e-8, "heat_alpha": 1.0, "heat_fourier": 0.2, "gamma": 1.4, "cfl": 0.4, "snapshot_every": 1}
+    c = sg.SolverConfig.from_json(j)
+    assert c.to_json() == dict(j, share=1.0)
+    with pytest.raises(sg.InvalidArgument):
+        sg.SolverConfig.from_json({"problem": "burgers"})
+
+
+def test_default_config_matches_reference(sg):
+    """config.hpp:29-48 via sg_config_default."""
+    from paper_2105_10332_b200 import _capi
+    c = _capi.sg_config()
+    _capi.load().sg_config_default(ctypes.byref(c))
+    assert (c.nx, c.block, c.steps, c.ranks, c.engine, c.mode) == (64, 8, 10, 1, 0, 0)
+    assert (c.share, c.heat_alpha, c.heat_fourier, c.gamma, c.cfl, c.cell_cost) == (1.0, 1.0, 0.2, 1.4, 0.4, 5e-8)
+    assert c.snapshot_every == 1
+
+
+def test_run_record_json_keys(sg):
+    rec = sg.RunRecord(engine="swept", problem="heat", ranks=2)
+    keys = list(rec.to_json())
+    assert keys == ["engine", "problem", "mode", "nx", "block", "ranks", "steps_requested", "actual_steps",
+                    "total_levels", "octahedra", "communicates", "dt", "setup_seconds", "wall_seconds",
+                    "modeled_seconds", "messages", "bytes", "cell_updates", "snapshot_frames", "per_rank"]
+    assert len(rec.to_json()["per_rank"]) == 2
