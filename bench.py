@@ -193,7 +193,7 @@ def main():
     ap.add_argument("--req-steps", type=int, default=REQ_STEPS)
     ap.add_argument("--per-gpu", type=int, default=PER_GPU)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
-    ap.add_argument("--no-extra", action="store_true", help="skip the Euler / standard side measurements")
+    ap.add_argument("--no-extra", action="store_true", help="skip the standard / Euler side measurements")
     ap.add_argument("--ref-sample-steps", type=int, default=21)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -209,70 +209,95 @@ def main():
     import paper_2105_10332_b200 as sg
 
     PER_GPU, REQ_STEPS = args.per_gpu, args.req_steps
+    dist = None
     if world > 1:
-        # one process per GPU: rank r owns partition r of the global grid.
-        # (Cross-process coupling: see DESIGN.md "multi-GPU"; this round the
-        # whole grid is driven by rank 0 over all visible devices.)
+        # one process per GPU: rank r owns partition r of the px x py grid;
+        # torch.distributed (NCCL) is plumbing only (IPC handle exchange,
+        # barriers, the max-over-ranks timing reduction)
         import torch.distributed as dist
-        torch.cuda.set_device(env_int("LOCAL_RANK", 0))
-        dist.init_process_group("nccl", init_method="env://")
-        if rank != 0:
-            dist.barrier()
-            dist.destroy_process_group()
-            return 0
-    n = args.gpus
+        # SG_BENCH_SAME_DEVICE=1 + SG_BENCH_BACKEND=gloo: exercise the N-rank
+        # path on a single GPU (all ranks share device 0; NCCL refuses that)
+        same = os.environ.get("SG_BENCH_SAME_DEVICE") == "1"
+        torch.cuda.set_device(0 if same else env_int("LOCAL_RANK", 0))
+        dist.init_process_group(os.environ.get("SG_BENCH_BACKEND", "nccl"), init_method="env://")
+    n = world if world > 1 else args.gpus
     px, py = GRIDS.get(n, (n, 1))
     nx, ny = PER_GPU * px, PER_GPU * py
-    base = dict(problem="heat", nx=nx, ny=ny, block=BLOCK, steps=REQ_STEPS, ranks=px * py, px=px, py=py, devices=n)
+    pw, ph = nx // px, ny // py
+    pi, pj = rank % px, rank // px
+    base = dict(problem="heat", nx=nx, ny=ny, block=BLOCK, steps=REQ_STEPS, ranks=px * py, px=px, py=py)
 
-    def timed(engine, profile):
-        cfg = sg.SolverConfig(engine=engine, **base)
-        s = sg.Solver(cfg, profile=profile)
+    def make(engine, profile=False, **over):
+        cfg = sg.SolverConfig(engine=engine, **dict(base, **over))
+        if dist is not None:
+            return sg.DistSolver(cfg, rank=rank, world=world, profile=profile)
+        return sg.Solver(cfg, profile=profile)
+
+    def sync():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed(engine, profile, **over):
+        s = make(engine, profile, **over)
         for _ in range(args.warmup):
             s.reset()
             s.solve()
-        torch.cuda.synchronize()
+        sync()
         dev, kst = [], []
         t0 = time.perf_counter()
         for _ in range(args.steps):
             s.reset()
             dev.append(s.solve())
             kst.append(s.kernel_stats())
-        torch.cuda.synchronize()
+        sync()
         wall = time.perf_counter() - t0
-        res = s.fetch()
-        return s, dev, kst, wall, res
+        return s, max_over_ranks(sum(dev)), kst, max_over_ranks(wall)
 
     clocks = Clocks()
-    clocks.start()
-    sw, sw_dev, sw_k, sw_wall, sw_res = timed("swept", True)
-    ck = clocks.stop()
-    updates = sw_res.record.cell_updates
-    dev_total = sum(sw_dev)
-    value = updates * args.steps / dev_total
+    if rank == 0:
+        clocks.start()
+    sw, sw_dev, sw_k, sw_wall = timed("swept", True)
+    ck = clocks.stop() if rank == 0 else None
+    rec = sw.fetch().record
+    updates = rec.cell_updates
+    value = updates * args.steps / sw_dev
 
-    # ---- e2e: pinned host in -> solve -> host out, every step --------------
+    # ---- e2e: pinned host piece in -> solve -> host piece out, every step --
     nv = 1
-    host_in = torch.empty((nv, ny, nx), dtype=torch.float64).pin_memory()
-    host_out = torch.empty((nv, ny, nx), dtype=torch.float64).pin_memory()
-    sw.initial(host_in)  # the reference initial condition (make_setup, engine.cpp:31-42)
-    for _ in range(1):
-        sw.upload(host_in)
-        sw.reset()
-        sw.solve()
-        sw.download(host_out)
-    torch.cuda.synchronize()
+    full = np.empty((nv, ny, nx))
+    sw.initial(full)  # the reference initial condition (make_setup, engine.cpp:31-42)
+    if dist is not None:
+        piece = full[:, pj * ph:(pj + 1) * ph, pi * pw:(pi + 1) * pw]
+    else:
+        piece = full
+    host_in = torch.from_numpy(np.ascontiguousarray(piece)).pin_memory()
+    host_out = torch.empty_like(host_in).pin_memory()
+    del full
+    sw.upload(host_in)
+    sw.reset()
+    sw.solve()
+    sw.download(host_out)
+    ref_out = host_out.numpy().copy()
+    sync()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         sw.upload(host_in)
         sw.reset()
         sw.solve()
         sw.download(host_out)
-    torch.cuda.synchronize()
-    e2e_wall = time.perf_counter() - t0
+    sync()
+    e2e_wall = max_over_ranks(time.perf_counter() - t0)
     e2e_value = updates * args.steps / e2e_wall
-    assert np.array_equal(host_out.numpy(), sw_res.final_field.data), "e2e output differs from resident solve"
-    launches = sw_res.record.kernel_launches * args.steps
+    assert np.array_equal(host_out.numpy(), ref_out), "e2e output differs between repeats"
+    launches = rec.kernel_launches * args.steps
 
     # ---- roofline of the dominant kernel (Octahedron phase) ----------------
     peaks, peak_kind = measured_peaks()
@@ -282,89 +307,83 @@ def main():
     achieved = per_launch_bytes / per_launch_s / 1e9
     tag = workload_config(n, nx, ny)["workload"]
     nt = ncu_traffic(tag)
-    roof = {"kernel": "swept_phase_kernel<heat> (Octahedron launches)", "bound": "hbm",
+    roof = {"kernel": "swept_heat_kernel (Octahedron launches)", "bound": "hbm",
             "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": nt[0] if nt else None,
-            "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else
+            "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else
             "fallback 6650 GB/s (B200_PROFILING.md)",
             "alg_bytes_per_launch": per_launch_bytes, "mean_launch_ms": per_launch_s * 1e3,
-            "launches_per_step": k["launches"], "share_of_step": round(k["seconds"] / sw_dev[-1], 4),
+            "launches_per_step": k["launches"], "share_of_step": round(k["seconds"] * args.steps / sw_dev, 4),
             "traffic_source": nt[1] if nt else None}
     sw.close()
 
-    # ---- standard engine on the same workload (speedup) --------------------
     extra = {}
-    st_value = None
     if not args.no_extra:
-        base_std = dict(base, steps=sw_res.record.actual_steps)
-        cfg = sg.SolverConfig(engine="standard", **base_std)
-        st = sg.Solver(cfg, profile=False)
-        for _ in range(args.warmup):
-            st.reset()
-            st.solve()
-        st_dev = []
-        for _ in range(args.steps):
-            st.reset()
-            st_dev.append(st.solve())
-        st_res = st.fetch()
-        st_value = st_res.record.cell_updates * args.steps / sum(st_dev)
-        same = bool(np.array_equal(st_res.final_field.data, sw_res.final_field.data))
+        # standard decomposition on the same workload (swept/standard speedup)
+        st, st_dev, _, _ = timed("standard", False, steps=rec.actual_steps)
+        st_rec = st.fetch().record
+        st_value = st_rec.cell_updates * args.steps / st_dev
         st.close()
-        extra["standard"] = {"value": st_value, "unit": "cell-updates/s", "ms_per_step": 1e3 * sum(st_dev) / args.steps,
-                             "bitwise_equal_to_swept": same}
+        extra["standard"] = {"value": st_value, "unit": "cell-updates/s", "ms_per_step": 1e3 * st_dev / args.steps}
         extra["swept_over_standard"] = value / st_value
-        # configs[1]: Euler 960^2 b16 swept vs standard (one GPU)
-        eu = {}
-        for eng in ("swept", "standard"):
-            steps_e = 500 if eng == "swept" else None
-            cfg = sg.SolverConfig(problem="euler", nx=960, block=16, engine=eng,
-                                  steps=steps_e or eu["swept"]["actual_steps"])
-            s = sg.Solver(cfg)
-            for _ in range(3):
-                s.reset()
-                s.solve()
-            ts = []
-            for _ in range(args.steps):
-                s.reset()
-                ts.append(s.solve())
-            r = s.fetch()
-            eu[eng] = {"value": r.record.cell_updates * args.steps / sum(ts), "actual_steps": r.record.actual_steps,
-                       "ms_per_step": 1e3 * sum(ts) / args.steps}
-            s.close()
-        eu["swept_over_standard"] = eu["swept"]["value"] / eu["standard"]["value"]
-        extra["euler_960_b16"] = eu
+        if n == 1:
+            # configs[1]: Euler 960^2 b16 swept vs standard (one GPU)
+            eu = {}
+            for eng in ("swept", "standard"):
+                cfg = sg.SolverConfig(problem="euler", nx=960, block=16, engine=eng,
+                                      steps=500 if eng == "swept" else eu["swept"]["actual_steps"])
+                s = sg.Solver(cfg)
+                for _ in range(3):
+                    s.reset()
+                    s.solve()
+                ts = []
+                for _ in range(args.steps):
+                    s.reset()
+                    ts.append(s.solve())
+                r = s.fetch()
+                eu[eng] = {"value": r.record.cell_updates * args.steps / sum(ts),
+                           "actual_steps": r.record.actual_steps, "ms_per_step": 1e3 * sum(ts) / args.steps}
+                if eng == "standard":
+                    eu["bitwise_equal"] = bool(np.array_equal(r.final_field.data, eu.pop("_field")))
+                else:
+                    eu["_field"] = r.final_field.data
+                s.close()
+            eu["swept_over_standard"] = eu["swept"]["value"] / eu["standard"]["value"]
+            extra["euler_960_b16"] = eu
 
     # ---- CPU baseline: the reference on this host, bounded sample ----------
     cpu = None
-    if not args.no_cpu and n == 1:
+    if not args.no_cpu and n == 1 and rank == 0:
         threads = os.cpu_count() or 1
-        v, rec = cpu_reference_sample(nx, ny, args.ref_sample_steps, "swept", threads)
+        v, crec = cpu_reference_sample(nx, ny, args.ref_sample_steps, "swept", threads)
         if v is not None:
-            cpu = {"value": v, "unit": "cell-updates/s", "cores": rec["cfg"]["ranks"], "kind": "reference",
-                   "sample": f"reference swept engine (oracle/_ref), heat {rec['cfg']['nx']}^2 b{BLOCK}, "
-                             f"{args.ref_sample_steps} requested steps ({rec['actual_steps']} actual), "
-                             f"{rec['cfg']['ranks']} ranks x 1 thread, wall {rec['median_wall_seconds']:.2f} s"}
-            vs, recs = cpu_reference_sample(nx, ny, args.ref_sample_steps, "standard", threads)
+            cpu = {"value": v, "unit": "cell-updates/s", "cores": crec["cfg"]["ranks"], "kind": "reference",
+                   "sample": f"reference swept engine (oracle/_ref), heat {crec['cfg']['nx']}^2 b{BLOCK}, "
+                             f"{args.ref_sample_steps} requested steps ({crec['actual_steps']} actual), "
+                             f"{crec['cfg']['ranks']} ranks x 1 thread, wall {crec['median_wall_seconds']:.2f} s"}
+            vs, _ = cpu_reference_sample(nx, ny, args.ref_sample_steps, "standard", threads)
             if vs is not None:
                 cpu["standard_value"] = vs
                 cpu["standard_sample"] = f"reference standard engine, 1 rank x {threads} OpenMP threads"
 
-    line = {
-        "metric": METRIC, "value": value, "unit": "cell-updates/s", "n_gpus": n, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * dev_total / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(n, nx, ny),
-        "e2e": {"value": e2e_value, "unit": "cell-updates/s", "h2d_bytes_per_step": nv * nx * ny * 8,
-                "d2h_bytes_per_step": nv * nx * ny * 8},
-        "gpu_launches": launches,
-        "roofline": roof, "cpu_baseline": cpu, "clocks": ck,
-        "actual_steps": sw_res.record.actual_steps, "cell_updates_per_step": updates,
-        "wall_ms_per_step": 1e3 * sw_wall / args.steps,
-    }
-    line.update(extra)
-    print(json.dumps(line))
-    if world > 1:
-        import torch.distributed as dist
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "cell-updates/s", "n_gpus": n, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * sw_dev / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(n, nx, ny),
+            "e2e": {"value": e2e_value, "unit": "cell-updates/s", "h2d_bytes_per_step": nv * nx * ny * 8,
+                    "d2h_bytes_per_step": nv * nx * ny * 8},
+            "gpu_launches": launches,
+            "roofline": roof, "cpu_baseline": cpu, "clocks": ck,
+            "actual_steps": rec.actual_steps, "cell_updates_per_step": updates,
+            "wall_ms_per_step": 1e3 * sw_wall / args.steps,
+            "multi_gpu": "one process per GPU; partition-edge records pushed by P2P stores from the phase "
+                         "kernels, launches ordered by device-side epoch flags" if n > 1 else None,
+        }
+        line.update(extra)
+        print(json.dumps(line))
+    if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
     return 0

@@ -132,7 +132,9 @@ int sg_solver_kernel_stats(sg_solver* s, int which, double* seconds, long* launc
                            double* alg_bytes, double* updates);
 /* Host-buffer I/O of the resident solver (the e2e path): upload replaces the
  * level-0 field with `host` ([var][ny][nx] fp64, pinned or pageable) and
- * download writes the final field into `host`; both synchronous. */
+ * download writes the final field into `host`; both synchronous.  A
+ * distributed solver (sg_dist_create) reads / writes only its own partition
+ * [var][ny/py][nx/px]. */
 int sg_solver_upload(sg_solver* s, const double* host, char* err, size_t errlen);
 int sg_solver_download(sg_solver* s, double* host, char* err, size_t errlen);
 /* The initial condition make_setup computed (engine.cpp:27-70), [var][ny][nx]. */
@@ -140,6 +142,23 @@ int sg_solver_initial(sg_solver* s, double* host, char* err, size_t errlen);
 /* Enable (1) / disable (0) per-launch CUDA events around the dominant kernel. */
 int sg_solver_set_profile(sg_solver* s, int on);
 void sg_solver_destroy(sg_solver* s);
+
+/* ------------------------------------------- one process per GPU (NVLink) --
+ * The distributed form of sg_solver_create for runs launched one process per
+ * GPU (torchrun): rank r owns partition r of the px*py grid (world == px*py)
+ * on its current CUDA device.  Its buffers are exported as CUDA IPC handles
+ * (sg_dist_blob); the caller all-gathers the blobs in rank order by any means
+ * (torch.distributed does it in the Python layer) and hands them to
+ * sg_dist_connect, after which kernels store partition-edge cells straight
+ * into the peers' memory over NVLink and dependent launches are ordered by
+ * device-side epoch flags (no host round trip).  This replaces the
+ * reference's Transport::exchange (transport.hpp:78-79).  reset / solve /
+ * upload / download / fetch then act on the local partition (fetch fills only
+ * this rank's part of final_field). */
+int sg_dist_create(const sg_config* cfg, int rank, int world, sg_solver** out, char* err, size_t errlen);
+/* Writes this rank's IPC blob into buf (if cap suffices); returns its size. */
+long sg_dist_blob(sg_solver* s, void* buf, long cap, char* err, size_t errlen);
+int sg_dist_connect(sg_solver* s, const void* blobs, long per_rank, char* err, size_t errlen);
 
 /* Swept plan introspection (host only, no GPU): compiles the phase plan of
  * build_schedule (geometry.cpp:169-184) for (problem, block, steps) and

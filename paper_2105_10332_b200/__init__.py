@@ -6,12 +6,12 @@ Public API mirrors the reference (see api.py for the file:line mapping):
 ``substep`` (the equation plugin on device buffers), ``max_levels``,
 ``build_schedule`` and the reference's exception types.
 """
-from .api import (CudaError, FieldState, InvalidArgument, LinkModel, LogicError, NonPhysicalState, PoolSpec,
+from .api import (CudaError, DistSolver, FieldState, InvalidArgument, LinkModel, LogicError, NonPhysicalState, PoolSpec,
                   RunRecord, RunResult, SnapshotIOError, Solver, SolverConfig, SweptError, TransportError,
-                  build_schedule, device_count, max_levels, plan_info, run, substep, version)
+                  build_schedule, device_count, max_levels, plan_info, run, run_distributed, substep, version)
 
 __all__ = [
-    "CudaError", "FieldState", "InvalidArgument", "LinkModel", "LogicError", "NonPhysicalState", "PoolSpec",
+    "CudaError", "DistSolver", "FieldState", "InvalidArgument", "LinkModel", "LogicError", "NonPhysicalState", "PoolSpec",
     "RunRecord", "RunResult", "SnapshotIOError", "Solver", "SolverConfig", "SweptError", "TransportError",
-    "build_schedule", "device_count", "max_levels", "plan_info", "run", "substep", "version",
+    "build_schedule", "device_count", "max_levels", "plan_info", "run", "run_distributed", "substep", "version",
 ]

@@ -51,7 +51,7 @@ EXPORTS = (
     "sg_config_default", "sg_validate", "sg_run", "sg_free_result", "sg_solver_create",
     "sg_solver_reset", "sg_solver_solve", "sg_solver_fetch", "sg_solver_kernel_stats",
     "sg_solver_upload", "sg_solver_download", "sg_solver_initial", "sg_solver_set_profile", "sg_solver_destroy", "sg_plan_info", "sg_max_levels", "sg_schedule",
-    "sg_substep", "sg_version", "sg_device_count",
+    "sg_substep", "sg_version", "sg_device_count", "sg_dist_create", "sg_dist_blob", "sg_dist_connect",
 )
 
 _lib = None
@@ -94,6 +94,10 @@ def load() -> C.CDLL:
     L.sg_substep.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
                              C.c_int, C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_double), C.c_void_p,
                              C.c_char_p, C.c_size_t]
+    L.sg_dist_create.argtypes = [cp, C.c_int, C.c_int, C.POINTER(sp), C.c_char_p, C.c_size_t]
+    L.sg_dist_blob.argtypes = [sp, C.c_void_p, C.c_long, C.c_char_p, C.c_size_t]
+    L.sg_dist_blob.restype = C.c_long
+    L.sg_dist_connect.argtypes = [sp, C.c_void_p, C.c_long, C.c_char_p, C.c_size_t]
     L.sg_version.argtypes = []
     L.sg_version.restype = C.c_char_p
     L.sg_device_count.argtypes = []

@@ -312,12 +312,16 @@ class Solver:
     """Resident solver (sg_solver_*): create once, then reset/solve/fetch.
     Used by bench.py to time the solve with inputs already in HBM."""
 
-    def __init__(self, cfg: SolverConfig, profile: bool = False):
+    def __init__(self, cfg: SolverConfig, profile: bool = False, _dist=None):
         self._L = _c.load()
         self._cfg = cfg._c()
         h = C.c_void_p()
         err = _c.errbuf()
-        _check(self._L.sg_solver_create(C.byref(self._cfg), C.byref(h), err, len(err)), err)
+        if _dist is None:
+            _check(self._L.sg_solver_create(C.byref(self._cfg), C.byref(h), err, len(err)), err)
+        else:
+            rank, world = _dist
+            _check(self._L.sg_dist_create(C.byref(self._cfg), rank, world, C.byref(h), err, len(err)), err)
         self._h = h
         if profile:
             self._L.sg_solver_set_profile(self._h, 1)
@@ -382,6 +386,70 @@ class Solver:
 
     def __exit__(self, *a):
         self.close()
+
+
+class DistSolver(Solver):
+    """One process per GPU (launched by torchrun): this rank owns partition
+    `rank` of the cfg.px x cfg.py grid (world size == px*py) on its current
+    CUDA device.  torch.distributed is plumbing only: it all-gathers the CUDA
+    IPC handles once; afterwards partition-edge cells travel as P2P stores
+    from inside the phase kernels and launches are ordered by device-side
+    flags (the reference's Transport::exchange, transport.hpp:78-79)."""
+
+    def __init__(self, cfg: SolverConfig, rank: int = None, world: int = None, group=None, profile: bool = False):
+        import torch.distributed as dist
+        rank = dist.get_rank(group) if rank is None else rank
+        world = dist.get_world_size(group) if world is None else world
+        if not cfg.px and not cfg.py:
+            cfg.px, cfg.py = world, 1
+        if cfg.ranks != cfg.px * cfg.py:
+            cfg.ranks = cfg.px * cfg.py
+        super().__init__(cfg, profile=profile, _dist=(rank, world))
+        self.rank, self.world, self.cfg = rank, world, cfg
+        err = _c.errbuf()
+        n = self._L.sg_dist_blob(self._h, None, 0, err, len(err))
+        if n < 0:
+            _check(-n, err)
+        buf = C.create_string_buffer(n)
+        self._L.sg_dist_blob(self._h, buf, n, err, len(err))
+        blobs = [None] * world
+        dist.all_gather_object(blobs, bytes(buf.raw), group=group)
+        allb = b"".join(blobs)
+        _check(self._L.sg_dist_connect(self._h, allb, n, err, len(err)), err)
+
+    def gather(self, dst: int = 0, group=None):
+        """Assemble the global final field on rank `dst` (None elsewhere)."""
+        import torch.distributed as dist
+        res = self.fetch()
+        pi, pj = self.rank % self.cfg.px, self.rank // self.cfg.px
+        pw, ph = res.final_field.nx // self.cfg.px, res.final_field.ny // self.cfg.py
+        piece = res.final_field.data[:, pj * ph:(pj + 1) * ph, pi * pw:(pi + 1) * pw].copy()
+        pieces = [None] * self.world if self.rank == dst else None
+        dist.gather_object(piece, pieces, dst=dst, group=group)
+        if self.rank != dst:
+            return None
+        full = np.zeros_like(res.final_field.data)
+        for q, pc in enumerate(pieces):
+            qi, qj = q % self.cfg.px, q // self.cfg.px
+            full[:, qj * ph:(qj + 1) * ph, qi * pw:(qi + 1) * pw] = pc
+        res.final_field.data = full
+        return res
+
+
+def run_distributed(cfg: SolverConfig, group=None) -> Optional[RunResult]:
+    """run() with one process per GPU (torchrun); RunResult on rank 0."""
+    import time as _t
+    s = DistSolver(cfg, group=group)
+    t0 = _t.perf_counter()
+    s.reset()
+    secs = s.solve()
+    out = s.gather(0, group=group)
+    wall = _t.perf_counter() - t0
+    s.close()
+    if out is not None:
+        out.record.wall_seconds = wall
+        out.record.solve_seconds = secs
+    return out
 
 
 # ------------------------------------------------------- geometry / plugin --

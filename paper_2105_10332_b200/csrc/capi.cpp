@@ -98,6 +98,38 @@ int sg_solver_create(const sg_config* cfg, sg_solver** out, char* err, size_t er
     });
 }
 
+int sg_dist_create(const sg_config* cfg, int rank, int world, sg_solver** out, char* err, size_t errlen) {
+    *out = nullptr;
+    return guard(err, errlen, [&] {
+        if (cfg->snapshot_path && cfg->snapshot_path[0])
+            sg::fail(SG_EINVAL, "snapshots are not supported by the distributed solver");
+        auto* h = new sg_solver{nullptr};
+        try {
+            h->s = new sg::Solver(*cfg, rank, world);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+long sg_dist_blob(sg_solver* s, void* buf, long cap, char* err, size_t errlen) {
+    long n = -1;
+    const int rc = guard(err, errlen, [&] {
+        const auto b = s->s->ipc_blob();
+        n = static_cast<long>(b.size());
+        if (buf && cap >= n) std::memcpy(buf, b.data(), b.size());
+    });
+    return rc == SG_OK ? n : -rc;
+}
+
+int sg_dist_connect(sg_solver* s, const void* blobs, long per_rank, char* err, size_t errlen) {
+    return guard(err, errlen, [&] {
+        s->s->connect(static_cast<const unsigned char*>(blobs), static_cast<std::size_t>(per_rank));
+    });
+}
+
 int sg_solver_reset(sg_solver* s, char* err, size_t errlen) {
     return guard(err, errlen, [&] { s->s->reset(); });
 }

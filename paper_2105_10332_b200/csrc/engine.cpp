@@ -35,7 +35,7 @@ T* dev_upload(DeviceCtx& d, const std::vector<T>& v) {
 
 }  // namespace
 
-Solver::Solver(const sg_config& cfg) : cfg_(cfg) {
+Solver::Solver(const sg_config& cfg, int rank, int world) : cfg_(cfg), rank_(rank), world_(world) {
     const auto t0 = std::chrono::steady_clock::now();
     setup_ = make_setup(cfg_);
     const Equation& eq = setup_.eq;
@@ -57,9 +57,16 @@ Solver::Solver(const sg_config& cfg) : cfg_(cfg) {
     if (ndev < 1) fail(SG_ECUDA, "no CUDA device visible (the GPU solver has no CPU fallback)");
     int use = cfg_.devices > 0 ? std::min(cfg_.devices, ndev) : ndev;
     use = std::min(use, nparts_);
+    int dev0 = 0;
+    if (dist()) {  // one process per GPU: this rank owns partition `rank` on its current device
+        if (world_ != nparts_) fail(SG_EINVAL, "distributed run: world size must equal px*py");
+        if (rank_ < 0 || rank_ >= world_) fail(SG_EINVAL, "distributed run: bad rank");
+        ck(cudaGetDevice(&dev0), "cudaGetDevice");
+        use = 1;
+    }
     devs_.resize(use);
     for (int d = 0; d < use; ++d) {
-        devs_[d].dev = d;
+        devs_[d].dev = dev0 + d;
         ck(cudaSetDevice(d), "cudaSetDevice");
         ck(cudaStreamCreateWithFlags(&devs_[d].stream, cudaStreamNonBlocking), "stream");
         ck(cudaEventCreate(&devs_[d].ev_start), "event");
@@ -69,9 +76,9 @@ Solver::Solver(const sg_config& cfg) : cfg_(cfg) {
         for (int e = 0; e < use; ++e)
             if (e != d) {
                 int can = 0;
-                cudaDeviceCanAccessPeer(&can, d, e);
+                cudaDeviceCanAccessPeer(&can, dev0 + d, dev0 + e);
                 if (can) {
-                    cudaError_t r = cudaDeviceEnablePeerAccess(e, 0);
+                    cudaError_t r = cudaDeviceEnablePeerAccess(dev0 + e, 0);
                     if (r != cudaSuccess && r != cudaErrorPeerAccessAlreadyEnabled)
                         ck(r, "cudaDeviceEnablePeerAccess");
                     cudaGetLastError();
@@ -83,9 +90,19 @@ Solver::Solver(const sg_config& cfg) : cfg_(cfg) {
         parts_[p].id = p;
         parts_[p].pi = p % px_;
         parts_[p].pj = p / px_;
-        // contiguous blocks of partitions per device
-        parts_[p].dev = static_cast<int>(static_cast<long>(p) * use / nparts_);
-        devs_[parts_[p].dev].parts.push_back(p);
+        // contiguous blocks of partitions per device; remote partitions (other
+        // ranks of a distributed run) have dev = -1 and IPC-mapped buffers
+        if (dist()) {
+            parts_[p].dev = p == rank_ ? 0 : -1;
+        } else {
+            parts_[p].dev = static_cast<int>(static_cast<long>(p) * use / nparts_);
+        }
+        if (parts_[p].dev >= 0) devs_[parts_[p].dev].parts.push_back(p);
+    }
+    if (dist()) {
+        DeviceCtx& d = devs_[0];
+        flags_ = dev_alloc<unsigned long long>(d, kMaxParts);
+        ck(cudaMemset(flags_, 0, kMaxParts * sizeof(unsigned long long)), "flags");
     }
 
     if (cfg_.engine == SG_SWEPT) {
@@ -100,12 +117,14 @@ Solver::Solver(const sg_config& cfg) : cfg_(cfg) {
             cell_updates_ += static_cast<long long>(plan_.updates_per_kind[l.kind]) *
                              (setup_.nx / cfg_.block) * (setup_.ny / cfg_.block);
         build_swept();
+        if (!dist()) finalize_swept();
     } else {
         actual_steps_ = cfg_.steps;
         total_levels_ = cfg_.steps * eq.substeps;
         final_level_ = total_levels_;
         cell_updates_ = total_levels_ * static_cast<long long>(setup_.nx) * setup_.ny;
         build_standard();
+        if (!dist()) finalize_standard();
     }
     for (auto& d : devs_) {
         ck(cudaSetDevice(d.dev), "cudaSetDevice");
@@ -119,6 +138,8 @@ Solver::~Solver() {
         cudaSetDevice(d.dev);
         cudaStreamSynchronize(d.stream);
         for (void* p : d.allocs) cudaFree(p);
+        for (void* p : ipc_open_) cudaIpcCloseMemHandle(p);
+        ipc_open_.clear();
         for (auto e : d.prof_ev) cudaEventDestroy(e);
         cudaEventDestroy(d.ev_start);
         cudaEventDestroy(d.ev_stop);
@@ -144,6 +165,7 @@ void Solver::build_swept() {
     threads_ = 128;
 
     for (auto& pb : parts_) {
+        if (pb.dev < 0) continue;
         DeviceCtx& d = devs_[pb.dev];
         pb.init = dev_alloc<double>(d, plane * nv);
         pb.out = dev_alloc<double>(d, plane * nv);
@@ -177,7 +199,13 @@ void Solver::build_swept() {
         bytes_ += static_cast<long long>(pushes) * P.kinds[l.kind].exp_cells.size() * nv * 8;
         if (pushes) messages_ += nparts_;
     }
+}
 
+void Solver::finalize_swept() {
+    const SweptPlan& P = plan_;
+    const int b = cfg_.block;
+    const int pbx = pw_ / b, pby = ph_ / b;
+    const int g = P.ghost, extw = pbx + 2 * g;
     for (auto& d : devs_) {
         ck(cudaSetDevice(d.dev), "cudaSetDevice");
         for (int kd = 0; kd < K_NKINDS; ++kd) {
@@ -363,6 +391,7 @@ void Solver::build_standard() {
     const int pitch = pw_ + 2 * n, rows = ph_ + 2 * n;
     const std::size_t gplane = static_cast<std::size_t>(pitch) * rows;
     for (auto& pb : parts_) {
+        if (pb.dev < 0) continue;
         DeviceCtx& d = devs_[pb.dev];
         pb.ring.resize(S + 1);
         for (int s = 0; s <= S; ++s) pb.ring[s] = dev_alloc<double>(d, gplane * nv);
@@ -382,6 +411,23 @@ void Solver::build_standard() {
         ck(cudaMemcpy(pb.init_ghosted, piece.data(), piece.size() * sizeof(double), cudaMemcpyHostToDevice),
            "init H2D");
     }
+    // ledger: 4 face strips per partition per level when neighbours differ
+    for (long l = 1; l <= final_level_; ++l)
+        for (int q = 0; q < nparts_; ++q) {
+            if (px_ > 1) {
+                messages_ += 2;
+                bytes_ += 2LL * ph_ * n * nv * 8;
+            }
+            if (py_ > 1) {
+                messages_ += 2;
+                bytes_ += 2LL * pw_ * n * nv * 8;
+            }
+        }
+    prof_kind_ = 100;  // std step
+}
+
+void Solver::finalize_standard() {
+    const int S = setup_.eq.substeps;
     for (auto& d : devs_) {
         ck(cudaSetDevice(d.dev), "cudaSetDevice");
         for (int phase = 0; phase <= S; ++phase) {
@@ -398,20 +444,6 @@ void Solver::build_standard() {
             d.d_std_out.push_back(dev_upload(d, o));
         }
     }
-    // ledger: 4 face strips per partition per level when neighbours differ
-    for (long l = 1; l <= final_level_; ++l)
-        for (const auto& pb : parts_) {
-            if (px_ > 1) {
-                messages_ += 2;
-                bytes_ += 2LL * ph_ * n * nv * 8;
-            }
-            if (py_ > 1) {
-                messages_ += 2;
-                bytes_ += 2LL * pw_ * n * nv * 8;
-            }
-            (void)pb;
-        }
-    prof_kind_ = 100;  // std step
 }
 
 void Solver::reset() {
@@ -424,6 +456,7 @@ void Solver::reset() {
         const std::size_t gplane =
             static_cast<std::size_t>(pw_ + 2 * eq.halo) * (ph_ + 2 * eq.halo) * eq.nvars;
         for (auto& pb : parts_) {
+            if (pb.dev < 0) continue;
             DeviceCtx& d = devs_[pb.dev];
             ck(cudaSetDevice(d.dev), "cudaSetDevice");
             ck(cudaMemcpyAsync(pb.ring[0], pb.init_ghosted, gplane * sizeof(double), cudaMemcpyDeviceToDevice,
@@ -463,7 +496,12 @@ double Solver::solve() {
         prof_i += 2;
     };
     // barrier between dependent launches on different GPUs
+    if (dist() && !connected_) fail(SG_ETRANSPORT, "distributed solver used before connect()");
     auto cross_sync = [&]() {
+        if (dist()) {
+            dist_barrier(devs_[0]);
+            return;
+        }
         if (!multi) return;
         for (auto& d : devs_) {
             cudaSetDevice(d.dev);
@@ -477,6 +515,7 @@ double Solver::solve() {
         cudaSetDevice(d.dev);
         ck(cudaEventRecord(d.ev_start, d.stream), "event");
     }
+    if (dist()) dist_barrier(devs_[0]);  // no rank starts writing into a peer still in its previous solve
     if (cfg_.engine == SG_SWEPT) {
         for (std::size_t li = 0; li < plan_.launches.size(); ++li) {
             const bool pr = profile && plan_.launches[li].kind == prof_kind_;
@@ -576,8 +615,89 @@ void Solver::check_error() {
         int e = 0;
         cudaSetDevice(d.dev);
         ck(cudaMemcpy(&e, d.d_err, sizeof(int), cudaMemcpyDeviceToHost), "err D2H");
+        if (e & 2) fail(SG_ETRANSPORT, "distributed barrier timed out waiting for a peer GPU");
         if (e) fail(SG_ENONPHYS, "non-physical state: rho <= 0 or p <= 0");
     }
+}
+
+// ---------------------------------------------------------- distributed --
+namespace {
+struct IpcBlob {
+    int rank, nbuf;
+    cudaIpcMemHandle_t h[40];
+};
+}  // namespace
+
+std::vector<unsigned char> Solver::ipc_blob() const {
+    if (!dist()) fail(SG_ELOGIC, "ipc_blob: not a distributed solver");
+    IpcBlob b;
+    std::memset(&b, 0, sizeof b);
+    b.rank = rank_;
+    const PartBuffers& pb = parts_[rank_];
+    std::vector<void*> bufs;
+    if (cfg_.engine == SG_SWEPT) {
+        for (double* r : pb.rec) bufs.push_back(r);
+        bufs.push_back(pb.init);
+        bufs.push_back(pb.out);
+    } else {
+        for (double* r : pb.ring) bufs.push_back(r);
+        bufs.push_back(pb.init_ghosted);
+    }
+    bufs.push_back(flags_);
+    if (bufs.size() > 40) fail(SG_ELOGIC, "ipc_blob: too many buffers");
+    b.nbuf = static_cast<int>(bufs.size());
+    cudaSetDevice(devs_[0].dev);
+    for (std::size_t i = 0; i < bufs.size(); ++i) ck(cudaIpcGetMemHandle(&b.h[i], bufs[i]), "cudaIpcGetMemHandle");
+    std::vector<unsigned char> out(sizeof b);
+    std::memcpy(out.data(), &b, sizeof b);
+    return out;
+}
+
+void Solver::connect(const unsigned char* blobs, std::size_t per_rank) {
+    if (!dist()) fail(SG_ELOGIC, "connect: not a distributed solver");
+    if (per_rank != sizeof(IpcBlob)) fail(SG_ETRANSPORT, "connect: peer blob size mismatch");
+    cudaSetDevice(devs_[0].dev);
+    peer_flags_.assign(world_, nullptr);
+    peer_flags_[rank_] = flags_;
+    for (int q = 0; q < world_; ++q) {
+        IpcBlob b;
+        std::memcpy(&b, blobs + q * per_rank, sizeof b);
+        if (b.rank != q) fail(SG_ETRANSPORT, "connect: blobs out of rank order");
+        if (q == rank_) continue;
+        std::vector<void*> p(b.nbuf, nullptr);
+        for (int i = 0; i < b.nbuf; ++i) {
+            ck(cudaIpcOpenMemHandle(&p[i], b.h[i], cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+            ipc_open_.push_back(p[i]);
+        }
+        PartBuffers& pb = parts_[q];
+        int i = 0;
+        if (cfg_.engine == SG_SWEPT) {
+            pb.rec.resize(plan_.nslots);
+            for (int s2 = 0; s2 < plan_.nslots; ++s2) pb.rec[s2] = static_cast<double*>(p[i++]);
+            pb.init = static_cast<double*>(p[i++]);
+            pb.out = static_cast<double*>(p[i++]);
+        } else {
+            pb.ring.resize(setup_.eq.substeps + 1);
+            for (auto& r : pb.ring) r = static_cast<double*>(p[i++]);
+            pb.init_ghosted = static_cast<double*>(p[i++]);
+        }
+        peer_flags_[q] = static_cast<unsigned long long*>(p[i++]);
+        if (i != b.nbuf) fail(SG_ETRANSPORT, "connect: peer buffer list mismatch");
+    }
+    d_peer_flags_ = dev_upload(devs_[0], peer_flags_);
+    if (cfg_.engine == SG_SWEPT) finalize_swept();
+    else finalize_standard();
+    ck(cudaDeviceSynchronize(), "connect sync");
+    connected_ = true;
+}
+
+cudaError_t launch_dist_barrier(unsigned long long* const* peer_flags, unsigned long long* my_flags, int world,
+                                int rank, unsigned long long epoch, int* err, cudaStream_t s);
+
+void Solver::dist_barrier(DeviceCtx& d) {
+    ++epoch_;
+    ck(launch_dist_barrier(d_peer_flags_, flags_, world_, rank_, epoch_, d.d_err, d.stream), "dist barrier");
+    ++launches_;
 }
 
 void Solver::fetch(sg_result* r) {
@@ -587,7 +707,9 @@ void Solver::fetch(sg_result* r) {
     double* field = static_cast<double*>(std::malloc(sizeof(double) * nv * nx * ny));
     if (!field) fail(SG_ELOGIC, "out of host memory");
     std::vector<double> piece;
+    if (dist()) std::memset(field, 0, sizeof(double) * nv * nx * ny);
     for (auto& pb : parts_) {
+        if (pb.dev < 0) continue;
         DeviceCtx& d = devs_[pb.dev];
         cudaSetDevice(d.dev);
         if (cfg_.engine == SG_SWEPT) {
@@ -640,14 +762,17 @@ void Solver::fetch(sg_result* r) {
 }
 
 void Solver::upload(const double* host) {
-    // Level 0 from a host field [var][ny][nx] (pinned host memory is DMA'd directly).
+    // Level 0 from a host field [var][ny][nx] (pinned host memory is DMA'd
+    // directly).  Distributed runs pass only this rank's piece [var][ph][pw].
     const Equation& eq = setup_.eq;
-    const std::size_t nx = setup_.nx, ny = setup_.ny;
+    const std::size_t nx = dist() ? pw_ : setup_.nx, ny = dist() ? ph_ : setup_.ny;
+    const int ox = dist() ? 0 : 1, oy = dist() ? 0 : 1;  // piece origin multiplier
     for (auto& pb : parts_) {
+        if (pb.dev < 0) continue;
         DeviceCtx& d = devs_[pb.dev];
         cudaSetDevice(d.dev);
         for (int v = 0; v < eq.nvars; ++v) {
-            const double* src = host + (v * ny + static_cast<std::size_t>(pb.pj) * ph_) * nx + pb.pi * pw_;
+            const double* src = host + (v * ny + static_cast<std::size_t>(oy * pb.pj) * ph_) * nx + ox * pb.pi * pw_;
             if (cfg_.engine == SG_SWEPT) {
                 ck(cudaMemcpy2DAsync(pb.init + static_cast<std::size_t>(v) * ph_ * pw_, pw_ * sizeof(double), src,
                                      nx * sizeof(double), pw_ * sizeof(double), ph_, cudaMemcpyHostToDevice,
@@ -656,6 +781,8 @@ void Solver::upload(const double* host) {
             } else {
                 const int n = eq.halo, pitch = pw_ + 2 * n, rows = ph_ + 2 * n;
                 double* dst = pb.init_ghosted + static_cast<std::size_t>(v) * pitch * rows;
+                if (dist()) fail(SG_EINVAL, "upload: the distributed standard engine takes its ghosts from peers; "
+                                            "upload is supported for the swept engine only");
                 auto copy = [&](int gx0, int gy0, int w, int h, int lx, int ly) {
                     // global window (wrapped start) -> local ghosted coords (lx, ly) in [-n, pw+n)
                     const int sx = ((gx0 % (int)nx) + (int)nx) % (int)nx, sy = ((gy0 % (int)ny) + (int)ny) % (int)ny;
@@ -681,12 +808,14 @@ void Solver::upload(const double* host) {
 
 void Solver::download(double* host) {
     const Equation& eq = setup_.eq;
-    const std::size_t nx = setup_.nx, ny = setup_.ny;
+    const std::size_t nx = dist() ? pw_ : setup_.nx, ny = dist() ? ph_ : setup_.ny;
+    const int ox = dist() ? 0 : 1, oy = dist() ? 0 : 1;
     for (auto& pb : parts_) {
+        if (pb.dev < 0) continue;
         DeviceCtx& d = devs_[pb.dev];
         cudaSetDevice(d.dev);
         for (int v = 0; v < eq.nvars; ++v) {
-            double* dst = host + (v * ny + static_cast<std::size_t>(pb.pj) * ph_) * nx + pb.pi * pw_;
+            double* dst = host + (v * ny + static_cast<std::size_t>(oy * pb.pj) * ph_) * nx + ox * pb.pi * pw_;
             if (cfg_.engine == SG_SWEPT) {
                 ck(cudaMemcpy2DAsync(dst, nx * sizeof(double), pb.out + static_cast<std::size_t>(v) * ph_ * pw_,
                                      pw_ * sizeof(double), pw_ * sizeof(double), ph_, cudaMemcpyDeviceToHost, d.stream),

@@ -60,7 +60,8 @@ struct DeviceCtx {
 
 class Solver {
   public:
-    explicit Solver(const sg_config& cfg);
+    // rank/world >= 0: distributed run, one process per GPU owning partition `rank`
+    explicit Solver(const sg_config& cfg, int rank = -1, int world = 0);
     ~Solver();
     void reset();
     double solve();  // device seconds (max over devices)
@@ -73,9 +74,18 @@ class Solver {
     double setup_seconds = 0.0;
     bool profile = false;
 
+    // distributed (one process per GPU): export this rank's buffers as CUDA
+    // IPC handles, then map every other rank's and build the kernel tables
+    std::vector<unsigned char> ipc_blob() const;
+    void connect(const unsigned char* blobs, std::size_t per_rank);
+    bool dist() const { return rank_ >= 0; }
+
   private:
     void build_swept();
     void build_standard();
+    void finalize_swept();
+    void finalize_standard();
+    void dist_barrier(DeviceCtx& d);
     void check_error();
 
     sg_config cfg_;
@@ -91,6 +101,13 @@ class Solver {
     std::vector<PartBuffers> parts_;
     std::vector<DeviceCtx> devs_;
     double last_solve_ = 0.0;
+    int rank_ = -1, world_ = 0;
+    bool connected_ = false;
+    unsigned long long* flags_ = nullptr;            // [kMaxParts] epochs signalled by each rank
+    std::vector<unsigned long long*> peer_flags_;     // every rank's flag array (IPC-mapped)
+    unsigned long long** d_peer_flags_ = nullptr;
+    unsigned long long epoch_ = 0;
+    std::vector<void*> ipc_open_;
     // profiling of the dominant kernel class
     int prof_kind_ = -1;
     double prof_seconds_ = 0.0;

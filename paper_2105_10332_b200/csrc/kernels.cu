@@ -630,7 +630,46 @@ __global__ void substep_rects_kernel(int stage, const double* __restrict__ r1, c
     }
 }
 
+// Cross-process barrier between dependent launches of a distributed run (one
+// process per GPU): publish this rank's epoch into every peer's flag array
+// (system-scope release after the previous kernel's P2P stores), then wait
+// until every peer has published the same epoch into ours.  Bounded: after
+// 60 s without progress it raises bit 1 of the error flag (TransportError)
+// instead of hanging the GPU.
+__global__ void dist_barrier_kernel(unsigned long long* const* peer_flags, unsigned long long* my_flags, int world,
+                                    int rank, unsigned long long epoch, int* err) {
+    if (threadIdx.x != 0) return;
+    __threadfence_system();
+    for (int q = 0; q < world; ++q) {
+        unsigned long long* f = peer_flags[q] + rank;
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(epoch) : "memory");
+    }
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (int q = 0; q < world; ++q) {
+        while (true) {
+            unsigned long long v;
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(my_flags + q) : "memory");
+            if (v >= epoch) break;
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t - t0 > 60ull * 1000000000ull) {
+                atomicOr(err, 2);
+                return;
+            }
+            __nanosleep(200);
+        }
+    }
+    __threadfence_system();
+}
+
 }  // namespace
+
+cudaError_t launch_dist_barrier(unsigned long long* const* peer_flags, unsigned long long* my_flags, int world,
+                                int rank, unsigned long long epoch, int* err, cudaStream_t s) {
+    dist_barrier_kernel<<<1, 32, 0, s>>>(peer_flags, my_flags, world, rank, epoch, err);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_swept(int problem, const SweptArgs& a, int G, int threads, cudaStream_t s) {
     const int ninst = a.pbx * a.pby;

@@ -1,0 +1,69 @@
+"""One process per partition (the torchrun layout) exercised on ONE GPU: two
+processes each own one partition of a 2x1 / 1x2 grid, exchange CUDA IPC
+handles through torch.distributed (gloo), push partition-edge cells into each
+other's buffers from inside the kernels and order launches with the
+device-side epoch barrier.  On a multi-GPU box the same code path uses
+NVLink P2P.  Result must equal the CPU oracle bit for bit."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, cfgd, q):
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    sys.path.insert(0, str(root))
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import paper_2105_10332_b200 as sg
+        res = sg.run_distributed(sg.SolverConfig(**cfgd))
+        if rank == 0:
+            q.put(("ok", res.final_field.data, res.final_field.level, res.record.messages))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # noqa: BLE001
+        q.put(("err", repr(e), None, None))
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("engine", ["swept", "standard"])
+@pytest.mark.parametrize("problem,px,py", [("heat", 2, 1), ("heat", 1, 2), ("euler", 2, 1)])
+def test_two_process_partitions_bitwise(sg, oracle, engine, problem, px, py):
+    if sg.device_count() < 1:
+        pytest.fail("no CUDA device")
+    import torch.multiprocessing as mp
+    nx = 64
+    cfgd = dict(problem=problem, nx=nx, block=16 if problem == "heat" else 8, steps=12, engine=engine,
+                ranks=px * py, px=px, py=py)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, cfgd, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    status, data, level, msgs = q.get(timeout=500)
+    for p in procs:
+        p.join(timeout=120)
+    assert status == "ok", data
+    P = oracle.HEAT if problem == "heat" else oracle.EULER
+    init, params = oracle.params(P, nx)
+    want = oracle.standard_solve(P, init, level, params)
+    assert np.array_equal(data, want)
+    assert msgs > 0
