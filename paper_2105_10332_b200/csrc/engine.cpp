@@ -8,7 +8,7 @@
 
 namespace sg {
 
-cudaError_t launch_swept(int problem, const SweptArgs& a, int G, int threads, cudaStream_t s);
+cudaError_t launch_swept(int problem, const SweptArgs& a, cudaStream_t s);
 cudaError_t launch_std(int problem, const StdArgs& a, cudaStream_t s);
 
 namespace {
@@ -157,12 +157,11 @@ void Solver::build_swept() {
     const std::size_t rec_len = static_cast<std::size_t>(extw) * exth * nv * P.max_epad;
     const std::size_t plane = static_cast<std::size_t>(pw_) * ph_;
 
-    // instances per CTA: keep ~<= 48 KB of smem per CTA, 1..8 instances
+    // one instance's phase must fit on chip (levels + Euler flux scratch)
     int inst_smem = 0;
     for (int kd = 0; kd < K_NKINDS; ++kd) inst_smem = std::max(inst_smem, P.kinds[kd].smem_doubles * 8);
-    G_ = std::max(1, std::min(8, (48 * 1024) / std::max(1, inst_smem)));
-    if (inst_smem * G_ > 200 * 1024) fail(SG_EINVAL, "swept: block too large for on-chip phases");
-    threads_ = 128;
+    if (inst_smem > 160 * 1024)
+        fail(SG_EINVAL, "swept: block too large for the on-chip phases (shared memory per instance)");
 
     for (auto& pb : parts_) {
         if (pb.dev < 0) continue;
@@ -224,33 +223,6 @@ void Solver::finalize_swept() {
             for (const auto& e : K.pitch) pt.push_back(make_int2(e[0], e[1]));
             d.d_lanes[kd] = dev_upload(d, ln);
             d.d_pitch[kd] = dev_upload(d, pt);
-            std::vector<DevCtaLevel> cl;
-            for (const auto& e : K.cta_levels) {
-                DevCtaLevel x{e[0], e[1], e[2], e[3], e[4], e[5], e[6], e[7], e[8], e[9],
-                              e[3] > 0 ? 1.0f / static_cast<float>(e[3]) : 0.0f, 0};
-                if (e[3] > 0 && e[4] == 0) fail(SG_EINVAL, "swept: phase rectangle wider than a CTA");
-                cl.push_back(x);
-            }
-            d.d_clev[kd] = dev_upload(d, cl);
-            std::vector<int2> el;
-            for (const auto& e : K.exp_lvl) el.push_back(make_int2(e[0], e[1]));
-            d.d_exp_lvl[kd] = dev_upload(d, el);
-            d.d_exp_begin[kd] = dev_upload(d, K.exp_begin);
-            std::vector<int4> tl;
-            for (const auto& e : K.tlanes) tl.push_back(make_int4(e[0], e[1], e[2], e[3]));
-            d.d_tlanes[kd] = dev_upload(d, tl);
-            std::vector<int4> cv;
-            int xb = 1 << 30;
-            for (int r = 1; r <= K.nlev; ++r) xb = std::min(xb, K.at(r).comp.x0);
-            for (int r = 1; r <= K.nlev; ++r) {
-                const PlanLevel& Lc = K.at(r);
-                const PlanLevel& Lp = K.at(r - 1);
-                cv.push_back(make_int4(Lc.comp.x0, Lc.comp.x1, Lc.comp.y0, Lc.comp.y1));
-                cv.push_back(make_int4(Lp.off - Lp.bbox.y0 * Lp.bbox.w() - Lp.bbox.x0, Lp.bbox.w(),
-                                       Lc.off - Lc.bbox.y0 * Lc.bbox.w() - Lc.bbox.x0, Lc.bbox.w()));
-            }
-            d.d_colv[kd] = dev_upload(d, cv);
-            d.xbase[kd] = K.nlev > 0 ? xb : 0;
         }
         for (const ClassTab& T : P.classes) {
             std::vector<int4> im, in;
@@ -261,10 +233,6 @@ void Solver::finalize_swept() {
                 im2.push_back(make_int2((x.seg << 20) | x.src, x.dst));
             }
             d.d_imp2.push_back(dev_upload(d, im2));
-            std::vector<int2> cp;
-            for (const auto& e : T.copies) cp.push_back(make_int2(e[0], e[1]));
-            d.d_copies.push_back(dev_upload(d, cp));
-            d.d_copy_begin.push_back(dev_upload(d, T.copy_begin));
             for (const InitImport& x : T.inits) in.push_back(make_int4(x.rx, x.ry, x.dst, x.vstride));
             d.d_imp.push_back(dev_upload(d, im));
             d.d_init.push_back(dev_upload(d, in));
@@ -310,31 +278,6 @@ void Solver::finalize_swept() {
             a.exp_vs = d.d_exp_vs[L.kind];
             a.lanes = d.d_lanes[L.kind];
             a.pitch = d.d_pitch[L.kind];
-            a.clev = d.d_clev[L.kind];
-            a.tw = K.tw;
-            a.tx0 = K.tx0;
-            a.ty0 = K.ty0;
-            a.tile_doubles = K.tw * K.th;
-            a.npacked = static_cast<int>(T.imports.size() + T.inits.size());
-            a.warp_doubles = a.npacked + 2 * a.tile_doubles;
-            a.warp_doubles += a.warp_doubles & 1;  // 16-byte aligned per warp
-            a.copies = d.d_copies[L.cls];
-            a.copy_begin = d.d_copy_begin[L.cls];
-            a.exp_lvl = d.d_exp_lvl[L.kind];
-            a.exp_begin = d.d_exp_begin[L.kind];
-            a.tlanes = d.d_tlanes[L.kind];
-            a.colv = d.d_colv[L.kind];
-            a.xbase = d.xbase[L.kind];
-            {
-                int cols = 0;
-                for (int kd = 0; kd < K_NKINDS; ++kd)
-                    for (int r = 1; r <= P.kinds[kd].nlev; ++r)
-                        cols = std::max(cols, P.kinds[kd].at(r).comp.x1 - d.xbase[kd]);
-                a.lpi = 1;
-                while (a.lpi < cols) a.lpi <<= 1;
-                if (a.lpi > 32) fail(SG_EINVAL, "swept: block wider than a warp (b - 2n > 32)");
-                a.lpi = std::max(a.lpi, 8);  // <= 4 instances per warp
-            }
             a.imports = d.d_imp[L.cls];
             a.imports2 = d.d_imp2[L.cls];
             a.nimp = static_cast<int>(T.imports.size());
@@ -522,7 +465,7 @@ double Solver::solve() {
             for (auto& d : devs_) {
                 if (multi) cudaSetDevice(d.dev);
                 if (&d == &d0) prof_begin(pr);
-                ck(launch_swept(prob, d.swept_args[li], G_, threads_, d.stream), "swept launch");
+                ck(launch_swept(prob, d.swept_args[li], d.stream), "swept launch");
                 if (&d == &d0) prof_end(pr);
                 ++launches_;
             }

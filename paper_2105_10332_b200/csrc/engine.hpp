@@ -38,14 +38,6 @@ struct DeviceCtx {
     int* d_exp_vs[K_NKINDS] = {};
     int4* d_lanes[K_NKINDS] = {};
     int2* d_pitch[K_NKINDS] = {};
-    DevCtaLevel* d_clev[K_NKINDS] = {};
-    int2* d_exp_lvl[K_NKINDS] = {};
-    int* d_exp_begin[K_NKINDS] = {};
-    int4* d_tlanes[K_NKINDS] = {};
-    int4* d_colv[K_NKINDS] = {};
-    int xbase[K_NKINDS] = {};
-    std::vector<int2*> d_copies;
-    std::vector<int*> d_copy_begin;
     std::vector<int4*> d_imp, d_init;
     std::vector<int2*> d_imp2;
     double** d_rec_tab = nullptr;
@@ -97,7 +89,6 @@ class Solver {
     long messages_ = 0;
     long long bytes_ = 0;
     long launches_ = 0;
-    int G_ = 1, threads_ = 128;
     std::vector<PartBuffers> parts_;
     std::vector<DeviceCtx> devs_;
     double last_solve_ = 0.0;

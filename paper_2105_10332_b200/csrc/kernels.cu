@@ -1,22 +1,23 @@
 // sm_100a kernels of the swept solver.
 //
-//  swept_phase_kernel<PROB>  one launch = one swept phase (UpPyramid, YBridge,
-//      XBridge, Octahedron = OctahedronDown+OctahedronUp, DownPyramid) for every
-//      block instance of the partitions on this GPU.  A CTA owns G instances:
+//  swept_heat_kernel / swept_euler_kernel: one launch = one swept phase
+//      (UpPyramid, YBridge, XBridge, Octahedron = OctahedronDown+OctahedronUp,
+//      DownPyramid) for every block instance of the partitions on this GPU:
 //        1. gather: imported edge cells (records of earlier phases, or the
-//           initial plane) -> shared memory, coalesced along the records;
-//        2. advance all levels of the phase on chip (the pyramid / bridge /
-//           octahedron), one __syncthreads per level;
+//           initial plane) -> shared memory (cp.async, straight to place);
+//        2. advance all levels of the phase on chip;
 //        3. scatter: the cells later phases read (this instance's record)
 //           -> HBM, plus the copies partition-edge instances push into the
 //           neighbouring partitions' ghost records (NVLink P2P stores when
 //           the neighbour is another GPU);
 //        4. cells at the output level -> the owning partition's output plane.
-//  std_step_kernel<PROB>     the standard decomposition: one sub-step over the
-//      whole partition, boundary cells pushed into the neighbours' ghost
-//      frames (replaces StandardRank::exchange_ghosts + compute,
-//      engine.cpp:351-408).
-//  substep_rects_kernel<PROB>  run_substep on rectangles (physics.cpp:551-575).
+//  std_heat_kernel / std_euler_kernel: the standard decomposition, one
+//      sub-step over the whole partition with boundary cells pushed into the
+//      neighbours' ghost frames (StandardRank::exchange_ghosts + compute,
+//      engine.cpp:351-408 of the reference).  std_step_kernel<PROB> is the
+//      point-wise fallback for odd partition widths.
+//  substep_rects_kernel<PROB>: run_substep on rectangles (physics.cpp:551-575).
+//  dist_barrier_kernel: cross-process launch ordering (one process per GPU).
 #include <cuda_runtime.h>
 
 #include "kernels.cuh"
@@ -29,139 +30,6 @@ namespace {
 __device__ __forceinline__ int wrapi(int v, int n) {
     v %= n;
     return v < 0 ? v + n : v;
-}
-
-template <int PROB>
-__global__ void __launch_bounds__(128) swept_phase_kernel(const __grid_constant__ SweptArgs A, int G) {
-    extern __shared__ double sm[];
-    constexpr int NV = PROB == 0 ? 1 : 4;
-    const int T = blockDim.x, tid = threadIdx.x;
-    const int ninst = A.pbx * A.pby;
-    const int batches = (ninst + G - 1) / G;
-    const int part = A.dev_parts[blockIdx.x / batches];
-    const int inst0 = (blockIdx.x % batches) * G;
-    const int pi = part % A.px, pj = part / A.px;
-    const int SD = A.smem_doubles;
-    const int half = A.frame * (A.b / 2);
-    int err = 0;
-
-    // ---- 1. gather -------------------------------------------------------
-    for (int e = tid; e < G * A.nimp; e += T) {
-        const int g = e / A.nimp, i = e - g * A.nimp;
-        const int inst = inst0 + g;
-        if (inst >= ninst) continue;
-        const int bi = inst % A.pbx, bj = inst / A.pbx;
-        const int4 im = __ldg(&A.imports[i]);
-        const DevSeg s = A.segs[im.x];
-        const long ext = (long)(bj + s.dj + A.ghost) * A.extw + (bi + s.di + A.ghost);
-        const double* src = A.rec[part * A.nslots + s.slot] + ext * NV * s.epad + im.y;
-        double* dst = sm + g * SD + im.z;
-#pragma unroll
-        for (int v = 0; v < NV; ++v) dst[v * im.w] = src[v * s.epad];
-    }
-    for (int e = tid; e < G * A.ninit; e += T) {
-        const int g = e / A.ninit, i = e - g * A.ninit;
-        const int inst = inst0 + g;
-        if (inst >= ninst) continue;
-        const int bi = inst % A.pbx, bj = inst / A.pbx;
-        const int4 im = __ldg(&A.inits[i]);
-        const int gx = wrapi(pi * A.pw + bi * A.b - half + im.x, A.nx);
-        const int gy = wrapi(pj * A.ph + bj * A.b - half + im.y, A.ny);
-        const int opi = gx / A.pw, opj = gy / A.ph;
-        const double* src = A.init_planes[opj * A.px + opi] + (long)(gy - opj * A.ph) * A.pw + (gx - opi * A.pw);
-        double* dst = sm + g * SD + im.z;
-        const long pl = (long)A.pw * A.ph;
-#pragma unroll
-        for (int v = 0; v < NV; ++v) dst[v * im.w] = src[v * pl];
-    }
-    __syncthreads();
-
-    // ---- 2. advance the phase on chip ------------------------------------
-    for (int r = 1; r <= A.nlev; ++r) {
-        const DevLevel Lc = A.lev[r - A.rmin];
-        const DevLevel Lp = A.lev[r - 1 - A.rmin];
-        const int cw = Lc.cx1 - Lc.cx0, ch = Lc.cy1 - Lc.cy0, cells = cw * ch;
-        int stage = 0;
-        DevLevel Lpp = Lp;
-        if (PROB == 1) {
-            stage = (A.stage0 + r - 1) & 1;
-            if (stage == 1) Lpp = A.lev[r - 2 - A.rmin];
-        }
-        for (int c = tid; c < G * cells; c += T) {
-            const int g = c / cells, rem = c - g * cells;
-            const int yy = rem / cw, xx = rem - yy * cw;
-            const int x = Lc.cx0 + xx, y = Lc.cy0 + yy;
-            if (inst0 + g >= ninst) continue;
-            double* base = sm + g * SD;
-            const double* sp = base + Lp.off + (y - Lp.by0) * Lp.bw + (x - Lp.bx0);
-            double* dp = base + Lc.off + (y - Lc.by0) * Lc.bw + (x - Lc.bx0);
-            double outv[NV];
-            if (PROB == 0) {
-                outv[0] = heat_update(sp[0], sp[1], sp[-1], sp[Lp.bw], sp[-Lp.bw], A.c0, A.c1);
-            } else {
-                double q0[4];
-                const double* bp =
-                    stage == 0 ? sp : base + Lpp.off + (y - Lpp.by0) * Lpp.bw + (x - Lpp.bx0);
-                const int bvs = stage == 0 ? Lp.vstride : Lpp.vstride;
-#pragma unroll
-                for (int v = 0; v < 4; ++v) q0[v] = bp[v * bvs];
-                const double cx = stage == 0 ? A.c1 : A.c3;
-                const double cy = stage == 0 ? A.c2 : A.c4;
-                const int pbw = Lp.bw, pvs = Lp.vstride;
-                euler_update_d([&](int dx, int dy, int v) { return sp[v * pvs + dy * pbw + dx]; }, q0, cx,
-                               cy, A.c0, outv, err);
-            }
-#pragma unroll
-            for (int v = 0; v < NV; ++v) dp[v * Lc.vstride] = outv[v];
-            if (r == A.r_out) {
-                const int inst = inst0 + g;
-                const int bi = inst % A.pbx, bj = inst / A.pbx;
-                const int gx = wrapi(pi * A.pw + bi * A.b - half + x, A.nx);
-                const int gy = wrapi(pj * A.ph + bj * A.b - half + y, A.ny);
-                const int opi = gx / A.pw, opj = gy / A.ph;
-                double* o = A.out_planes[opj * A.px + opi] + (long)(gy - opj * A.ph) * A.pw + (gx - opi * A.pw);
-                const long pl = (long)A.pw * A.ph;
-#pragma unroll
-                for (int v = 0; v < NV; ++v) o[v * pl] = outv[v];
-            }
-        }
-        __syncthreads();
-    }
-
-    // ---- 3. scatter the record (+ ghost pushes at partition edges) ------
-    if (A.nexp > 0) {
-        for (int e = tid; e < G * A.nexp; e += T) {
-            const int g = e / A.nexp, i = e - g * A.nexp;
-            const int inst = inst0 + g;
-            if (inst >= ninst) continue;
-            const int bi = inst % A.pbx, bj = inst / A.pbx;
-            const int so = __ldg(&A.exp_off[i]), vs = __ldg(&A.exp_vs[i]);
-            double val[NV];
-#pragma unroll
-            for (int v = 0; v < NV; ++v) val[v] = sm[g * SD + so + v * vs];
-            {
-                const long ext = (long)(bj + A.ghost) * A.extw + (bi + A.ghost);
-                double* d = A.rec[part * A.nslots + A.my_slot] + ext * NV * A.epad + i;
-#pragma unroll
-                for (int v = 0; v < NV; ++v) d[v * A.epad] = val[v];
-            }
-            const int gh = A.ghost;
-            if (bi < gh || bi >= A.pbx - gh || bj < gh || bj >= A.pby - gh) {
-                for (int ej = -1; ej <= 1; ++ej)
-                    for (int ei = -1; ei <= 1; ++ei) {
-                        if (ei == 0 && ej == 0) continue;
-                        const int tbi = bi - ei * A.pbx, tbj = bj - ej * A.pby;
-                        if (tbi < -gh || tbi >= A.pbx + gh || tbj < -gh || tbj >= A.pby + gh) continue;
-                        const int tp = wrapi(pj + ej, A.py) * A.px + wrapi(pi + ei, A.px);
-                        const long ext = (long)(tbj + gh) * A.extw + (tbi + gh);
-                        double* d = A.rec[tp * A.nslots + A.my_slot] + ext * NV * A.epad + i;
-#pragma unroll
-                        for (int v = 0; v < NV; ++v) d[v * A.epad] = val[v];
-                    }
-            }
-        }
-    }
-    if (err) *A.err = 1;
 }
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
@@ -671,7 +539,7 @@ cudaError_t launch_dist_barrier(unsigned long long* const* peer_flags, unsigned 
     return cudaGetLastError();
 }
 
-cudaError_t launch_swept(int problem, const SweptArgs& a, int G, int threads, cudaStream_t s) {
+cudaError_t launch_swept(int problem, const SweptArgs& a, cudaStream_t s) {
     const int ninst = a.pbx * a.pby;
     if (problem == 0) {
         const size_t per_inst = static_cast<size_t>(a.smem_doubles) * sizeof(double);
@@ -694,18 +562,6 @@ cudaError_t launch_swept(int problem, const SweptArgs& a, int G, int threads, cu
         swept_euler_kernel<<<grid, 128, smem, s>>>(a);
         return cudaGetLastError();
     }
-    const int grid = a.ndev_parts * ((ninst + G - 1) / G);
-    const size_t smem = static_cast<size_t>(G) * a.smem_doubles * sizeof(double);
-    if (problem == 0) {
-        if (smem > 48 * 1024)
-            cudaFuncSetAttribute(swept_phase_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        swept_phase_kernel<0><<<grid, threads, smem, s>>>(a, G);
-    } else {
-        if (smem > 48 * 1024)
-            cudaFuncSetAttribute(swept_phase_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        swept_phase_kernel<1><<<grid, threads, smem, s>>>(a, G);
-    }
-    return cudaGetLastError();
 }
 
 cudaError_t launch_std(int problem, const StdArgs& a, cudaStream_t s) {

@@ -15,13 +15,6 @@ struct DevLevel {
     int cx0, cx1, cy0, cy1; // computed rect (empty for r <= 0)
 };
 
-struct DevCtaLevel {         // CTA lane map of one computed level (heat)
-    int cx0, cy0, cy1, w, items, rps;
-    int poff, pbw, doff, cbw;   // src(x,y) = poff + y*pbw + x; dst = doff + y*cbw + x
-    float inv_w;
-    int pad;
-};
-
 struct DevSeg {
     int slot;   // record slot of the producer launch
     int di, dj;
@@ -39,19 +32,6 @@ struct SweptArgs {
     const int* exp_vs;       // [nexp]
     const int4* lanes;       // [nlev][32] warp lane map (heat)
     const int2* pitch;       // [nlev] {bbox width at r-1, at r}
-    const DevCtaLevel* clev; // [nlev] CTA lane map (heat)
-    // ping-pong tile kernels
-    int tw, tile_doubles, npacked, warp_doubles;
-    const int2* copies;      // class: {packed idx, tile off}
-    const int* copy_begin;   // class: [nlev - rmin + 2]
-    const int2* exp_lvl;     // kind: {tile off, record idx}
-    const int* exp_begin;    // kind: [nlev - rmin + 2]
-    const int4* tlanes;      // kind: [nlev][32] {tile off, rows, x, y0}
-    // column kernel: per computed level r, 2 x int4:
-    // {cx0, cx1, cy0, cy1}, {poff, pbw, doff, cbw}
-    const int4* colv;
-    int lpi, xbase;          // lanes per instance (pow2), tile column of lane 0
-    int tx0, ty0;            // tile origin (instance coords)
     // class tables
     const int4* imports;     // {seg, src, dst, vstride}
     const int2* imports2;    // {seg << 20 | src, dst}  (same entries, compact)

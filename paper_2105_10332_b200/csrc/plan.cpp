@@ -289,20 +289,6 @@ SweptPlan compile_swept_plan(int b, const Equation& eq, long m, long final_level
             K.exp_vstride.push_back(pl.vstride);
         }
         K.epad = static_cast<int>((K.exp_cells.size() + 3) / 4 * 4);
-        // CTA lane map for 128 threads: (column, row-chunk) items
-        for (int r = 1; r <= K.nlev; ++r) {
-            const PlanLevel& Lc = K.at(r);
-            const PlanLevel& Lp = K.at(r - 1);
-            const int w = Lc.comp.w(), h = Lc.comp.h();
-            const int T = 128;
-            int splits = std::max(1, std::min(h, T / std::max(1, w)));
-            const int rps = (h + splits - 1) / splits;
-            splits = (h + rps - 1) / rps;
-            const int items = w <= T ? w * splits : 0;
-            K.cta_levels.push_back({Lc.comp.x0, Lc.comp.y0, Lc.comp.y1, w, items, rps,
-                                    Lp.off - Lp.bbox.y0 * Lp.bbox.w() - Lp.bbox.x0, Lp.bbox.w(),
-                                    Lc.off - Lc.bbox.y0 * Lc.bbox.w() - Lc.bbox.x0, Lc.bbox.w()});
-        }
         // warp lane map: (column, row-chunk) items of each computed rectangle;
         // the row split divides the height exactly when it can, so every
         // active lane runs the same trip count (no divergent row loops)
@@ -438,66 +424,6 @@ SweptPlan compile_swept_plan(int b, const Equation& eq, long m, long final_level
     P.ghost = ghost;
     for (std::size_t i = 0; i < P.launches.size(); ++i)
         if (P.kinds[P.launches[i].kind].epad > 0) P.launches[i].slot = static_cast<int>(i % P.nslots);
-    // ------------------------------------------------ ping-pong tile maps --
-    for (int kd = 0; kd < K_NKINDS; ++kd) {
-        KindLayout& K = P.kinds[kd];
-        Rect t{1 << 30, -(1 << 30), 1 << 30, -(1 << 30)};
-        for (const PlanLevel& pl : K.lev) {
-            if (pl.bbox.empty()) continue;
-            t.x0 = std::min(t.x0, pl.bbox.x0);
-            t.x1 = std::max(t.x1, pl.bbox.x1);
-            t.y0 = std::min(t.y0, pl.bbox.y0);
-            t.y1 = std::max(t.y1, pl.bbox.y1);
-        }
-        K.tx0 = t.x0;
-        K.ty0 = t.y0;
-        K.tw = t.w() | 1;  // odd pitch: row chunks of a warp land on different banks
-        K.th = t.h();
-        std::vector<std::array<int, 3>> el;  // {r, tile off, rec idx}
-        for (std::size_t i = 0; i < K.exp_cells.size(); ++i) {
-            const auto& c = K.exp_cells[i];
-            el.push_back({c[0], K.tile_off(c[1], c[2]), static_cast<int>(i)});
-        }
-        std::stable_sort(el.begin(), el.end(), [](const auto& a, const auto& c) { return a[0] < c[0]; });
-        K.exp_begin.assign(K.nlev - K.rmin + 2, 0);
-        for (const auto& e : el) {
-            K.exp_lvl.push_back({e[1], e[2]});
-            ++K.exp_begin[e[0] - K.rmin + 1];
-        }
-        for (std::size_t i = 1; i < K.exp_begin.size(); ++i) K.exp_begin[i] += K.exp_begin[i - 1];
-        for (int r = 1; r <= K.nlev; ++r) {
-            const Rect c = K.at(r).comp;
-            const int w = c.w(), h = c.h();
-            const int splits = w >= 32 ? 1 : std::max(1, std::min(h, 32 / std::max(1, w)));
-            const int rps = (h + splits - 1) / splits;
-            for (int l = 0; l < 32; ++l) {
-                std::array<int, 4> e{0, 0, 0, 0};
-                if (w <= 32 && l < w * splits) {
-                    const int x = c.x0 + l % w, y0 = c.y0 + (l / w) * rps;
-                    const int rows = std::max(0, std::min(rps, c.y1 - y0));
-                    if (rows > 0) e = {K.tile_off(x, y0), rows, x, y0};
-                }
-                K.tlanes.push_back(e);
-            }
-        }
-    }
-    for (ClassTab& T : P.classes) {
-        const KindLayout& K = P.kinds[T.kind];
-        std::vector<std::array<int, 3>> cl;  // {r, packed idx, tile off}
-        for (std::size_t i = 0; i < T.imports.size(); ++i)
-            cl.push_back({T.imports[i].r, static_cast<int>(i), K.tile_off(T.imports[i].qx, T.imports[i].qy)});
-        for (std::size_t i = 0; i < T.inits.size(); ++i)
-            cl.push_back({T.inits[i].r, static_cast<int>(T.imports.size() + i),
-                          K.tile_off(T.inits[i].rx, T.inits[i].ry)});
-        std::stable_sort(cl.begin(), cl.end(), [](const auto& a, const auto& c) { return a[0] < c[0]; });
-        T.copy_begin.assign(K.nlev - K.rmin + 2, 0);
-        for (const auto& e : cl) {
-            if (e[0] < K.rmin || e[0] > K.nlev) fail(SG_ELOGIC, "plan: import level outside kind");
-            T.copies.push_back({e[1], e[2]});
-            ++T.copy_begin[e[0] - K.rmin + 1];
-        }
-        for (std::size_t i = 1; i < T.copy_begin.size(); ++i) T.copy_begin[i] += T.copy_begin[i - 1];
-    }
     for (const ClassTab& T : P.classes)
         P.imports_per_kind[T.kind] =
             std::max<long>(P.imports_per_kind[T.kind], static_cast<long>(T.imports.size() + T.inits.size()));

@@ -51,19 +51,6 @@ struct KindLayout {
     // rows = 0 for idle lanes.  pitch[r-1] = {bbox width at r-1, at r}.
     std::vector<std::array<int, 4>> lanes;
     std::vector<std::array<int, 2>> pitch;
-    // CTA lane map (heat kernel, T threads): per computed level r
-    // {cx0, cy0, cy1, w, items, rps, poff, pbw, doff, cbw} with
-    // src(x,y) = poff + y*pbw + x, dst(x,y) = doff + y*cbw + x.
-    std::vector<std::array<int, 10>> cta_levels;
-    // ping-pong tile: one rectangle holding any level's resident cells
-    int tx0 = 0, ty0 = 0, tw = 0, th = 0;
-    int tile_off(int x, int y) const { return (y - ty0) * tw + (x - tx0); }
-    // exports grouped by level: exp_lvl[exp_begin[r-rmin] .. exp_begin[r-rmin+1]) = {tile offset, record index}
-    std::vector<std::array<int, 2>> exp_lvl;
-    std::vector<int> exp_begin;
-    // warp lane map on the tile: per level r (1..nlev) x 32 lanes
-    // {tile offset of the first cell, rows, x, y0}
-    std::vector<std::array<int, 4>> tlanes;
     const PlanLevel& at(int r) const { return lev[r - rmin]; }
 };
 
@@ -89,12 +76,6 @@ struct ClassTab {
     std::vector<Segment> segs;
     std::vector<Import> imports;       // sorted by (seg, src)
     std::vector<InitImport> inits;
-    // ping-pong kernels: the gather lands in a packed area (record imports at
-    // [0, nimp), initial-plane imports at [nimp, nimp+ninit)); before level r+1
-    // the imports of level r move into the tile: copies[copy_begin[r-rmin] ..
-    // copy_begin[r-rmin+1]) = {packed index, tile offset}.
-    std::vector<std::array<int, 2>> copies;
-    std::vector<int> copy_begin;
 };
 
 struct Launch {
