@@ -162,6 +162,8 @@ void Solver::build_swept() {
     for (int kd = 0; kd < K_NKINDS; ++kd) inst_smem = std::max(inst_smem, P.kinds[kd].smem_doubles * 8);
     if (inst_smem > 160 * 1024)
         fail(SG_EINVAL, "swept: block too large for the on-chip phases (shared memory per instance)");
+    if (setup_.eq.problem == SG_HEAT && b != 8 && b != 12 && b != 16 && b != 24 && b != 32)
+        fail(SG_EINVAL, "swept heat: block must be one of 8, 12, 16, 24, 32 on the GPU");
 
     for (auto& pb : parts_) {
         if (pb.dev < 0) continue;
@@ -212,7 +214,7 @@ void Solver::finalize_swept() {
             if (K.nlev > kMaxLevels - 2) fail(SG_EINVAL, "swept: too many levels per phase");
             std::vector<DevLevel> lv;
             for (const PlanLevel& pl : K.lev)
-                lv.push_back({pl.bbox.x0, pl.bbox.y0, pl.bbox.w(), pl.bbox.h(), pl.off, pl.vstride, pl.comp.x0,
+                lv.push_back({pl.bbox.x0, pl.bbox.y0, pl.pitch, pl.bbox.h(), pl.off, pl.vstride, pl.comp.x0,
                               pl.comp.x1, pl.comp.y0, pl.comp.y1});
             d.d_lev[kd] = dev_upload(d, lv);
             d.d_exp_off[kd] = dev_upload(d, K.exp_off);
@@ -322,6 +324,37 @@ void Solver::finalize_swept() {
                 a.c4 = setup_.cy_corr;
             }
             a.err = d.d_err;
+            for (int r = 1; r <= K.nlev; ++r) {  // heat lane map: (column, row-chunk) items of a warp
+                const PlanLevel& Lc = K.at(r);
+                const PlanLevel& Lp = K.at(r - 1);
+                const int w = Lc.comp.w(), h = Lc.comp.h();
+                const int cap = w >= 32 ? 1 : std::max(1, std::min(h, 32 / std::max(1, w)));
+                int splits = 1;
+                for (int dd = cap; dd >= 1; --dd)
+                    if (h % dd == 0) {
+                        splits = dd;
+                        break;
+                    }
+                if (2 * splits < cap) splits = cap;
+                const int rps = (h + splits - 1) / splits;
+                splits = (h + rps - 1) / rps;
+                HeatLevel hl;
+                hl.cx0 = Lc.comp.x0;
+                hl.cy0 = Lc.comp.y0;
+                hl.cy1 = Lc.comp.y1;
+                hl.w = w;
+                hl.items = w <= 32 ? w * splits : 0;
+                hl.rps = rps;
+                hl.poff = Lp.off - Lp.bbox.y0 * Lp.pitch - Lp.bbox.x0;
+                hl.pbw = Lp.pitch;
+                hl.doff = Lc.off - Lc.bbox.y0 * Lc.pitch - Lc.bbox.x0;
+                hl.cbw = Lc.pitch;
+                hl.inv_w = w > 0 ? 1.0f / static_cast<float>(w) : 0.0f;
+                hl.pad = 0;
+                if (setup_.eq.problem == SG_HEAT && w > 32)
+                    fail(SG_EINVAL, "swept heat: phase rectangle wider than a warp (block > 34)");
+                a.hl[r - 1] = hl;
+            }
             d.swept_args.push_back(a);
         }
     }

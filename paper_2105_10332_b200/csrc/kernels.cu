@@ -132,18 +132,25 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_kernel(const __grid_const
             }
     };
 
-    // ---- 2. levels
+    // ---- 2. levels (per-level parameters come from the parameter block)
     const double fx = A.c0, fy = A.c1;
     for (int r = 1; r <= A.nlev; ++r) {
-        const int4 t = __ldg(&A.lanes[(r - 1) * 32 + lane]);
-        const int2 pt = __ldg(&A.pitch[r - 1]);
-        const int bp = pt.x, bc = pt.y;
-        const double* P = S + t.x;
-        double* D = S + t.y;
-        int n = t.z;
+        const HeatLevel& L = A.hl[r - 1];
+        const int bp = L.pbw, bc = L.cbw;
+        int x = 0, y0 = 0, n = 0;
+        if (lane < L.items) {
+            // item -> (column, row chunk); exact (items < 2^5, w <= 2^5)
+            const int ch = __float2int_rz((lane + 0.5f) * L.inv_w);
+            x = L.cx0 + (lane - ch * L.w);
+            y0 = L.cy0 + ch * L.rps;
+            n = min(L.rps, L.cy1 - y0);
+        }
         if (n > 0) {
+            const double* P = S + L.poff + y0 * bp + x;
+            double* D = S + L.doff + y0 * bc + x;
             double south = P[-bp], c = P[0];
-            for (; n >= 4; n -= 4) {
+            int m = n;
+            for (; m >= 4; m -= 4) {
                 const double n1 = P[bp], n2 = P[2 * bp], n3 = P[3 * bp], n4 = P[4 * bp];
                 const double v1 = heat_update(c, P[1], P[-1], n1, south, fx, fy);
                 const double v2 = heat_update(n1, P[bp + 1], P[bp - 1], n2, c, fx, fy);
@@ -158,23 +165,27 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_kernel(const __grid_const
                 P += 4 * bp;
                 D += 4 * bc;
             }
-            for (; n > 0; --n) {
-                const double nn = P[bp];
-                D[0] = heat_update(c, P[1], P[-1], nn, south, fx, fy);
-                south = c;
-                c = nn;
-                P += bp;
-                D += bc;
+            if (m >= 2) {
+                const double n1 = P[bp], n2 = P[2 * bp];
+                const double v1 = heat_update(c, P[1], P[-1], n1, south, fx, fy);
+                const double v2 = heat_update(n1, P[bp + 1], P[bp - 1], n2, c, fx, fy);
+                D[0] = v1;
+                D[bc] = v2;
+                south = n1;
+                c = n2;
+                P += 2 * bp;
+                D += 2 * bc;
+                m -= 2;
             }
-        }
-        if (r == A.r_out && t.z > 0) {
-            const int x = t.w & 0xFFFF, y0 = t.w >> 16;
-            const double* Dv = S + t.y;
-            for (int y = y0; y < y0 + t.z; ++y, Dv += bc) {
-                const int gx = wrapi(pi * A.pw + bi * A.b - half + x, A.nx);
-                const int gy = wrapi(pj * A.ph + bj * A.b - half + y, A.ny);
-                const int opi = gx / A.pw, opj = gy / A.ph;
-                A.out_planes[opj * A.px + opi][(long)(gy - opj * A.ph) * A.pw + (gx - opi * A.pw)] = *Dv;
+            if (m) D[0] = heat_update(c, P[1], P[-1], P[bp], south, fx, fy);
+            if (r == A.r_out) {
+                const double* Dv = S + L.doff + y0 * bc + x;
+                for (int y = y0; y < y0 + n; ++y, Dv += bc) {
+                    const int gx = wrapi(pi * A.pw + bi * A.b - half + x, A.nx);
+                    const int gy = wrapi(pj * A.ph + bj * A.b - half + y, A.ny);
+                    const int opi = gx / A.pw, opj = gy / A.ph;
+                    A.out_planes[opj * A.px + opi][(long)(gy - opj * A.ph) * A.pw + (gx - opi * A.pw)] = *Dv;
+                }
             }
         }
         __syncwarp();
@@ -572,7 +583,8 @@ cudaError_t launch_std(int problem, const StdArgs& a, cudaStream_t s) {
         return cudaGetLastError();
     }
     if (problem == 1) {
-        constexpr int TX = 32, TY = 8;
+        // 32 x 7: the fused flux step has 7*33 + 8*32 = 487 items = two rounds of 256
+        constexpr int TX = 32, TY = 7;
         dim3 grid((a.pw + TX - 1) / TX, (a.ph + TY - 1) / TY, a.ndev_parts);
         std_euler_kernel<TX, TY><<<grid, 256, 0, s>>>(a);
         return cudaGetLastError();

@@ -21,6 +21,15 @@ struct DevSeg {
     int epad;   // producer record length
 };
 
+// Uniform per-level parameters of the heat phase kernel, kept in the kernel's
+// parameter block (constant-cache broadcast, no dependent global loads).
+struct HeatLevel {
+    int cx0, cy0, cy1, w, items, rps;
+    int poff, pbw, doff, cbw;   // src(x,y) = poff + y*pbw + x; dst(x,y) = doff + y*cbw + x
+    float inv_w;
+    int pad;
+};
+
 // One swept phase launch (all partitions resident on one device).
 struct SweptArgs {
     // kind layout
@@ -52,6 +61,7 @@ struct SweptArgs {
     double c0, c1, c2, c3;           // heat: fx, fy | euler: gamma, cx, cy (per stage)
     double c4, c5;
     int* err;
+    HeatLevel hl[kMaxLevels];        // heat kernel: levels 1..nlev
 };
 
 // One standard sub-step (all partitions on one device); planes carry a

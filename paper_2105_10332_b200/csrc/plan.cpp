@@ -251,7 +251,8 @@ SweptPlan compile_swept_plan(int b, const Equation& eq, long m, long final_level
             auto it = box.find(r);
             if (it != box.end()) pl.bbox = it->second;
             pl.off = off;
-            pl.vstride = static_cast<int>(pl.bbox.area());
+            pl.pitch = pl.bbox.w();
+            pl.vstride = pl.bbox.h() * pl.pitch;
             if (r >= 1) pl.comp = kind_rect(kd, b, n, k, r);
             off += pl.vstride * P.nvars;
             K.lev.push_back(pl);
@@ -285,7 +286,7 @@ SweptPlan compile_swept_plan(int b, const Equation& eq, long m, long final_level
             if (r < K.rmin || r > K.nlev) fail(SG_ELOGIC, "plan: export outside kind levels");
             const PlanLevel& pl = K.at(r);
             K.exp_cells.push_back({r, x, y});
-            K.exp_off.push_back(pl.off + (y - pl.bbox.y0) * pl.bbox.w() + (x - pl.bbox.x0));
+            K.exp_off.push_back(pl.off + (y - pl.bbox.y0) * pl.pitch + (x - pl.bbox.x0));
             K.exp_vstride.push_back(pl.vstride);
         }
         K.epad = static_cast<int>((K.exp_cells.size() + 3) / 4 * 4);
@@ -296,7 +297,7 @@ SweptPlan compile_swept_plan(int b, const Equation& eq, long m, long final_level
             const PlanLevel& Lc = K.at(r);
             const PlanLevel& Lp = K.at(r - 1);
             const int w = Lc.comp.w(), h = Lc.comp.h();
-            K.pitch.push_back({Lp.bbox.w(), Lc.bbox.w()});
+            K.pitch.push_back({Lp.pitch, Lc.pitch});
             const int cap = w >= 32 ? 1 : std::max(1, std::min(h, 32 / std::max(1, w)));
             int splits = 1;
             for (int d = cap; d >= 1; --d)
@@ -313,8 +314,8 @@ SweptPlan compile_swept_plan(int b, const Equation& eq, long m, long final_level
                     const int x = Lc.comp.x0 + xi, y0 = Lc.comp.y0 + ch * rps;
                     const int rows = std::max(0, std::min(rps, Lc.comp.y1 - y0));
                     if (rows > 0) {
-                        e[0] = Lp.off + (y0 - Lp.bbox.y0) * Lp.bbox.w() + (x - Lp.bbox.x0);
-                        e[1] = Lc.off + (y0 - Lc.bbox.y0) * Lc.bbox.w() + (x - Lc.bbox.x0);
+                        e[0] = Lp.off + (y0 - Lp.bbox.y0) * Lp.pitch + (x - Lp.bbox.x0);
+                        e[1] = Lc.off + (y0 - Lc.bbox.y0) * Lc.pitch + (x - Lc.bbox.x0);
                         e[2] = rows;
                         e[3] = (x & 0xFFFF) | ((y0 & 0xFFFF) << 16);
                     }
@@ -343,7 +344,7 @@ SweptPlan compile_swept_plan(int b, const Equation& eq, long m, long final_level
         std::map<std::tuple<int, int, int, int>, int> seg_id;
         for (const RImport& im : rep_imports[L]) {
             const PlanLevel& pl = K.at(im.r);
-            const int dst = pl.off + (im.qy - pl.bbox.y0) * pl.bbox.w() + (im.qx - pl.bbox.x0);
+            const int dst = pl.off + (im.qy - pl.bbox.y0) * pl.pitch + (im.qx - pl.bbox.x0);
             if (im.delta == 0) {
                 InitImport ii;
                 ii.rx = im.qx;

@@ -27,7 +27,8 @@ namespace sg {
 struct PlanLevel {   // one relative level r of a kind, r in [rmin, nlev]
     Rect bbox;       // cells resident in smem at this level (instance coords)
     int off = 0;     // smem offset (doubles) of var 0; var v at off + v*vstride
-    int vstride = 0; // bbox area
+    int vstride = 0; // bbox rows * pitch
+    int pitch = 0;   // row pitch in doubles (>= bbox width; uniform b+1 for heat)
     Rect comp;       // computed cells (empty for r <= 0)
 };
 
