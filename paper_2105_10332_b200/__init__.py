@@ -7,11 +7,11 @@ Public API mirrors the reference (see api.py for the file:line mapping):
 ``build_schedule`` and the reference's exception types.
 """
 from .api import (CudaError, DistSolver, FieldState, InvalidArgument, LinkModel, LogicError, NonPhysicalState, PoolSpec,
-                  RunRecord, RunResult, SnapshotIOError, Solver, SolverConfig, SweptError, TransportError,
+                  RunRecord, RunResult, SnapshotFrame, SnapshotIOError, SnapshotReader, Solver, SolverConfig, SweptError, TransportError,
                   build_schedule, device_count, max_levels, plan_info, run, run_distributed, substep, version)
 
 __all__ = [
     "CudaError", "DistSolver", "FieldState", "InvalidArgument", "LinkModel", "LogicError", "NonPhysicalState", "PoolSpec",
-    "RunRecord", "RunResult", "SnapshotIOError", "Solver", "SolverConfig", "SweptError", "TransportError",
+    "RunRecord", "RunResult", "SnapshotFrame", "SnapshotIOError", "SnapshotReader", "Solver", "SolverConfig", "SweptError", "TransportError",
     "build_schedule", "device_count", "max_levels", "plan_info", "run", "run_distributed", "substep", "version",
 ]

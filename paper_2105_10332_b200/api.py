@@ -452,6 +452,53 @@ def run_distributed(cfg: SolverConfig, group=None) -> Optional[RunResult]:
     return out
 
 
+# --------------------------------------------------------------- snapshots --
+_MAGIC = b"SWPT2D\0\0"
+
+
+@dataclass
+class SnapshotFrame:  # snapshot.hpp:199-202
+    level: int
+    data: np.ndarray  # (nvars, ny, nx)
+
+
+class SnapshotReader:
+    """SWPT2D v1 reader (snapshot.cpp:86-115): magic, u32 version, u64 header
+    length, JSON header, then (u64 level, f64[var][y][x]) frames."""
+
+    def __init__(self, path: str):
+        import struct
+        try:
+            raw = open(path, "rb").read()
+        except OSError as e:
+            raise SnapshotIOError(f"snapshot: cannot open {path}") from e
+        if raw[:8] != _MAGIC:
+            raise SnapshotIOError("snapshot: bad magic")
+        (version,) = struct.unpack_from("<I", raw, 8)
+        if version != 1:
+            raise SnapshotIOError("snapshot: unsupported version")
+        (hlen,) = struct.unpack_from("<Q", raw, 12)
+        if 20 + hlen > len(raw):
+            raise SnapshotIOError("snapshot: truncated header")
+        self._meta = json.loads(raw[20:20 + hlen].decode())
+        m = self._meta
+        plane = m["nvars"] * m["nx"] * m["ny"]
+        off, self._frames = 20 + hlen, []
+        while off < len(raw):
+            if off + 8 + 8 * plane > len(raw):
+                raise SnapshotIOError("snapshot: truncated frame")
+            (level,) = struct.unpack_from("<Q", raw, off)
+            data = np.frombuffer(raw, dtype="<f8", count=plane, offset=off + 8).reshape(m["nvars"], m["ny"], m["nx"])
+            self._frames.append(SnapshotFrame(int(level), data.copy()))
+            off += 8 + 8 * plane
+
+    def meta(self) -> dict:
+        return self._meta
+
+    def frames(self) -> list:
+        return self._frames
+
+
 # ------------------------------------------------------- geometry / plugin --
 def max_levels(b: int, n: int) -> int:
     """geometry.cpp:59-66; raises InvalidArgument like the reference."""

@@ -85,8 +85,6 @@ int sg_validate(const sg_config* cfg, char* err, size_t errlen) {
 int sg_solver_create(const sg_config* cfg, sg_solver** out, char* err, size_t errlen) {
     *out = nullptr;
     return guard(err, errlen, [&] {
-        if (cfg->snapshot_path && cfg->snapshot_path[0])
-            sg::fail(SG_EINVAL, "snapshots are not supported by this build yet");
         auto* h = new sg_solver{nullptr};
         try {
             h->s = new sg::Solver(*cfg);
@@ -180,8 +178,6 @@ void sg_solver_destroy(sg_solver* s) {
 int sg_run(const sg_config* cfg, sg_result* out, char* err, size_t errlen) {
     std::memset(out, 0, sizeof *out);
     return guard(err, errlen, [&] {
-        if (cfg->snapshot_path && cfg->snapshot_path[0])
-            sg::fail(SG_EINVAL, "snapshots are not supported by this build yet");
         sg::Solver solver(*cfg);
         const auto t0 = std::chrono::steady_clock::now();
         solver.reset();

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstring>
+#include <memory>
 #include <string>
 
 namespace sg {
@@ -38,6 +39,12 @@ T* dev_upload(DeviceCtx& d, const std::vector<T>& v) {
 Solver::Solver(const sg_config& cfg, int rank, int world) : cfg_(cfg), rank_(rank), world_(world) {
     const auto t0 = std::chrono::steady_clock::now();
     setup_ = make_setup(cfg_);
+    if (cfg_.snapshot_path && cfg_.snapshot_path[0]) {
+        if (dist()) fail(SG_EINVAL, "snapshots are not supported by the distributed solver");
+        snap_path_ = cfg_.snapshot_path;
+        snap_every_ = cfg_.snapshot_every;
+    }
+    cfg_.snapshot_path = nullptr;  // the caller's string may not outlive us
     const Equation& eq = setup_.eq;
     px_ = cfg_.px;
     py_ = cfg_.py;
@@ -165,9 +172,28 @@ void Solver::build_swept() {
     if (setup_.eq.problem == SG_HEAT && b != 8 && b != 12 && b != 16 && b != 24 && b != 32)
         fail(SG_EINVAL, "swept heat: block must be one of 8, 12, 16, 24, 32 on the GPU");
 
+    if (!snap_path_.empty()) {
+        // level l is complete after the last launch computing it; frames are
+        // drained right then, so the ring needs the widest window of levels
+        // that are touched but not yet complete
+        const long flat = P.flat;
+        std::vector<long> last(flat + 1, -1);
+        for (std::size_t i = 0; i < P.launches.size(); ++i)
+            for (long l = P.launches[i].lo; l <= P.launches[i].hi; ++l) last[l] = static_cast<long>(i);
+        done_after_.assign(P.launches.size(), {});
+        for (long l = 1; l <= flat; ++l) done_after_[last[l]].push_back(l);
+        long lowest = 1, highest = 0, width = 1;
+        for (std::size_t i = 0; i < P.launches.size(); ++i) {
+            highest = std::max(highest, P.launches[i].hi);
+            width = std::max(width, highest - lowest + 1);
+            for (long l : done_after_[i]) lowest = std::max(lowest, l + 1);
+        }
+        frame_ring_ = static_cast<int>(width);
+    }
     for (auto& pb : parts_) {
         if (pb.dev < 0) continue;
         DeviceCtx& d = devs_[pb.dev];
+        if (frame_ring_ > 0) pb.frames = dev_alloc<double>(d, static_cast<std::size_t>(frame_ring_) * plane * nv);
         pb.init = dev_alloc<double>(d, plane * nv);
         pb.out = dev_alloc<double>(d, plane * nv);
         pb.rec.resize(P.nslots);
@@ -250,6 +276,9 @@ void Solver::finalize_swept() {
         d.d_rec_tab = dev_upload(d, rt);
         d.d_init_tab = dev_upload(d, it);
         d.d_out_tab = dev_upload(d, ot);
+        std::vector<double*> ft(nparts_, nullptr);
+        for (const auto& pb : parts_) ft[pb.id] = pb.frames;
+        d.d_frames_tab = dev_upload(d, ft);
 
         for (std::size_t li = 0; li < P.launches.size(); ++li) {
             const Launch& L = P.launches[li];
@@ -324,6 +353,10 @@ void Solver::finalize_swept() {
                 a.c4 = setup_.cy_corr;
             }
             a.err = d.d_err;
+            a.frames = d.d_frames_tab;
+            a.snap_every = frame_ring_ > 0 ? static_cast<int>(snap_every_) : 0;
+            a.frame_ring = std::max(1, frame_ring_);
+            a.lo = L.lo;
             for (int r = 1; r <= K.nlev; ++r) {  // heat lane map: (column, row-chunk) items of a warp
                 const PlanLevel& Lc = K.at(r);
                 const PlanLevel& Lp = K.at(r - 1);
@@ -492,6 +525,22 @@ double Solver::solve() {
         ck(cudaEventRecord(d.ev_start, d.stream), "event");
     }
     if (dist()) dist_barrier(devs_[0]);  // no rank starts writing into a peer still in its previous solve
+    std::unique_ptr<SnapshotWriter> writer;
+    if (!snap_path_.empty()) {  // FrameSink, engine.cpp:75-117 of the reference
+        SnapshotMeta m;
+        m.problem = setup_.eq.problem == SG_HEAT ? "heat" : "euler";
+        m.nx = setup_.nx;
+        m.ny = setup_.ny;
+        m.nvars = setup_.eq.nvars;
+        m.block = cfg_.block;
+        m.dt = setup_.dt;
+        m.dx = setup_.dx;
+        m.dy = setup_.dy;
+        m.alpha = cfg_.heat_alpha;
+        m.gamma = cfg_.gamma;
+        writer = std::make_unique<SnapshotWriter>(snap_path_, m);
+        writer->append_frame(0, setup_.initial.data());  // level 0 % every == 0
+    }
     if (cfg_.engine == SG_SWEPT) {
         for (std::size_t li = 0; li < plan_.launches.size(); ++li) {
             const bool pr = profile && plan_.launches[li].kind == prof_kind_;
@@ -513,6 +562,9 @@ double Solver::solve() {
                 prof_updates_ += inst * plan_.updates_per_kind[L.kind];
             }
             cross_sync();
+            if (writer)
+                for (long l : done_after_[li])
+                    if (l % snap_every_ == 0) snapshot_frame(*writer, l, static_cast<int>(l % frame_ring_));
         }
     } else {
         const Equation& eq = setup_.eq;
@@ -562,6 +614,7 @@ double Solver::solve() {
                 prof_updates_ += cells;
             }
             cross_sync();
+            if (writer && l % snap_every_ == 0) snapshot_frame(*writer, l, static_cast<int>(l % (S + 1)));
         }
     }
     double worst = 0.0;
@@ -582,8 +635,47 @@ double Solver::solve() {
         prof_seconds_ += ms * 1e-3;
     }
     last_solve_ = worst;
+    if (writer) {
+        writer->flush();
+        snapshot_frames_ = writer->frames();
+    }
     check_error();
     return worst;
+}
+
+void Solver::snapshot_frame(SnapshotWriter& w, long level, int slot) {
+    // gather one complete level from every partition (FrameCollector,
+    // snapshot.cpp:122-153) and append it
+    const Equation& eq = setup_.eq;
+    const int nv = eq.nvars;
+    const std::size_t nx = setup_.nx, ny = setup_.ny, plane = static_cast<std::size_t>(pw_) * ph_;
+    std::vector<double> full(nv * nx * ny), piece;
+    for (auto& pb : parts_) {
+        if (pb.dev < 0) continue;
+        DeviceCtx& d = devs_[pb.dev];
+        cudaSetDevice(d.dev);
+        ck(cudaStreamSynchronize(d.stream), "snapshot sync");
+        if (cfg_.engine == SG_SWEPT) {
+            piece.resize(plane * nv);
+            ck(cudaMemcpy(piece.data(), pb.frames + static_cast<std::size_t>(slot) * plane * nv,
+                          piece.size() * sizeof(double), cudaMemcpyDeviceToHost),
+               "snapshot D2H");
+            for (int v = 0; v < nv; ++v)
+                for (int y = 0; y < ph_; ++y)
+                    std::memcpy(&full[(v * ny + pb.pj * ph_ + y) * nx + pb.pi * pw_],
+                                &piece[(static_cast<std::size_t>(v) * ph_ + y) * pw_], sizeof(double) * pw_);
+        } else {
+            const int n = eq.halo, pitch = pw_ + 2 * n, rows = ph_ + 2 * n;
+            piece.resize(static_cast<std::size_t>(pitch) * rows * nv);
+            ck(cudaMemcpy(piece.data(), pb.ring[slot], piece.size() * sizeof(double), cudaMemcpyDeviceToHost),
+               "snapshot D2H");
+            for (int v = 0; v < nv; ++v)
+                for (int y = 0; y < ph_; ++y)
+                    std::memcpy(&full[(v * ny + pb.pj * ph_ + y) * nx + pb.pi * pw_],
+                                &piece[(static_cast<std::size_t>(v) * rows + y + n) * pitch + n], sizeof(double) * pw_);
+        }
+    }
+    w.append_frame(level, full.data());
 }
 
 void Solver::check_error() {
@@ -734,6 +826,7 @@ void Solver::fetch(sg_result* r) {
     r->bytes = bytes_;
     r->cell_updates = cell_updates_;
     r->kernel_launches = launches_;
+    r->snapshot_frames = snapshot_frames_;
     r->final_field = field;
 }
 

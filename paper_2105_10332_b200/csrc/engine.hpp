@@ -10,6 +10,7 @@
 
 #include "kernels.cuh"
 #include "plan.hpp"
+#include "snapshot.hpp"
 #include "sg_internal.hpp"
 
 namespace sg {
@@ -23,6 +24,8 @@ struct PartBuffers {
     // standard
     std::vector<double*> ring;          // [S+1] ghosted planes
     double* init_ghosted = nullptr;     // resident ghosted copy of level 0
+    // snapshots (swept): ring of frame planes [slot][var][ph][pw]
+    double* frames = nullptr;
 };
 
 struct DeviceCtx {
@@ -41,6 +44,7 @@ struct DeviceCtx {
     std::vector<int4*> d_imp, d_init;
     std::vector<int2*> d_imp2;
     double** d_rec_tab = nullptr;
+    double** d_frames_tab = nullptr;
     const double** d_init_tab = nullptr;
     double** d_out_tab = nullptr;
     std::vector<const double**> d_std_r1, d_std_r2;
@@ -99,6 +103,13 @@ class Solver {
     unsigned long long** d_peer_flags_ = nullptr;
     unsigned long long epoch_ = 0;
     std::vector<void*> ipc_open_;
+    // snapshots (SWPT2D, snapshot.cpp of the reference)
+    std::string snap_path_;
+    long snap_every_ = 1;
+    int frame_ring_ = 0;
+    std::vector<std::vector<long>> done_after_;  // swept: levels completed by launch i
+    long snapshot_frames_ = 0;
+    void snapshot_frame(SnapshotWriter& w, long level, int slot_or_ring);  // D2H + assemble + append
     // profiling of the dominant kernel class
     int prof_kind_ = -1;
     double prof_seconds_ = 0.0;

@@ -178,13 +178,18 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_kernel(const __grid_const
                 m -= 2;
             }
             if (m) D[0] = heat_update(c, P[1], P[-1], P[bp], south, fx, fy);
-            if (r == A.r_out) {
+            const long lev = A.lo + r - 1;
+            const bool snap = A.snap_every > 0 && lev % A.snap_every == 0;
+            if (r == A.r_out || snap) {
                 const double* Dv = S + L.doff + y0 * bc + x;
+                const long pl = (long)A.pw * A.ph;
                 for (int y = y0; y < y0 + n; ++y, Dv += bc) {
                     const int gx = wrapi(pi * A.pw + bi * A.b - half + x, A.nx);
                     const int gy = wrapi(pj * A.ph + bj * A.b - half + y, A.ny);
                     const int opi = gx / A.pw, opj = gy / A.ph;
-                    A.out_planes[opj * A.px + opi][(long)(gy - opj * A.ph) * A.pw + (gx - opi * A.pw)] = *Dv;
+                    const long o = (long)(gy - opj * A.ph) * A.pw + (gx - opi * A.pw);
+                    if (r == A.r_out) A.out_planes[opj * A.px + opi][o] = *Dv;
+                    if (snap) A.frames[opj * A.px + opi][(lev % A.frame_ring) * pl + o] = *Dv;
                 }
             }
         }
@@ -281,18 +286,28 @@ __global__ void __launch_bounds__(128) swept_euler_kernel(const __grid_constant_
         auto Q = [&](int x, int y, int v) { return S[Lp.off + v * Lp.vstride + (y - Lp.by0) * Lp.bw + (x - Lp.bx0)]; };
         auto B = [&](int x, int y, int v) { return S[Lb.off + v * Lb.vstride + (y - Lb.by0) * Lb.bw + (x - Lb.bx0)]; };
         const bool out = r == A.r_out;
+        const long lev = A.lo + r - 1;
+        const bool snap = A.snap_every > 0 && lev % A.snap_every == 0;
         auto O = [&](int x, int y, const double o[4]) {
             double* d = S + Lc.off + (y - Lc.by0) * Lc.bw + (x - Lc.bx0);
 #pragma unroll
             for (int v = 0; v < 4; ++v) d[v * Lc.vstride] = o[v];
-            if (out) {
+            if (out || snap) {
                 const int gx = wrapi(pi * A.pw + bi * A.b - half + x, A.nx);
                 const int gy = wrapi(pj * A.ph + bj * A.b - half + y, A.ny);
                 const int opi = gx / A.pw, opj = gy / A.ph;
-                double* g = A.out_planes[opj * A.px + opi] + (long)(gy - opj * A.ph) * A.pw + (gx - opi * A.pw);
                 const long pl = (long)A.pw * A.ph;
+                const long oo = (long)(gy - opj * A.ph) * A.pw + (gx - opi * A.pw);
+                if (out) {
+                    double* g = A.out_planes[opj * A.px + opi] + oo;
 #pragma unroll
-                for (int v = 0; v < 4; ++v) g[v * pl] = o[v];
+                    for (int v = 0; v < 4; ++v) g[v * pl] = o[v];
+                }
+                if (snap) {
+                    double* g = A.frames[opj * A.px + opi] + (lev % A.frame_ring) * 4 * pl + oo;
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) g[v * pl] = o[v];
+                }
             }
         };
         euler_rect(tid, T, Lc.cx0, Lc.cx1, Lc.cy0, Lc.cy1, Q, B, O, ps, fxs, fys, A.c0, stage == 0 ? A.c1 : A.c3,

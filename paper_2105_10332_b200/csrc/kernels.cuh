@@ -61,6 +61,11 @@ struct SweptArgs {
     double c0, c1, c2, c3;           // heat: fx, fy | euler: gamma, cx, cy (per stage)
     double c4, c5;
     int* err;
+    // snapshots: every computed cell of a level l with l % snap_every == 0 also
+    // goes to frame slot l % frame_ring of the owning partition
+    double* const* frames;           // [part] -> frame_ring planes [var][ph][pw]
+    int snap_every, frame_ring;
+    long lo;                         // absolute level of relative level 1
     HeatLevel hl[kMaxLevels];        // heat kernel: levels 1..nlev
 };
 

@@ -68,6 +68,22 @@ def main():
                 continue
             sched.append({"b": b, "n": n, "S": S, "steps": steps, **meta, "entries": len(rows)})
     out["schedule"] = sched
+    # SWPT2D snapshot streams written by the reference (snapshot.cpp:57-84)
+    import hashlib
+    import tempfile
+    snaps = []
+    for cfg in ({"problem": "heat", "nx": 32, "block": 8, "steps": 10},                 # test_engine.cpp:234-267
+                {"problem": "heat", "nx": 32, "block": 8, "steps": 6, "engine": "standard", "ranks": 2},
+                {"problem": "euler", "nx": 32, "block": 16, "steps": 5},                # odd flat level
+                {"problem": "euler", "nx": 48, "block": 8, "steps": 4, "snapshot_every": 3},
+                {"problem": "heat", "nx": 48, "block": 16, "steps": 30, "snapshot_every": 4}):
+        with tempfile.TemporaryDirectory() as td:
+            path = f"{td}/snap.bin"
+            field, rec = ref.run(dict(cfg, snapshot=path))
+            data = open(path, "rb").read()
+        snaps.append({"cfg": cfg, "sha256": hashlib.sha256(data).hexdigest(), "bytes": len(data),
+                      "frames": rec["snapshot_frames"], "total_levels": rec["total_levels"]})
+    out["snapshots"] = snaps
     (HERE / "golden.json").write_text(json.dumps(out, indent=1) + "\n")
     print("wrote", HERE / "golden.json")
 
