@@ -32,6 +32,27 @@ __device__ __forceinline__ int wrapi(int v, int n) {
     return v < 0 ? v + n : v;
 }
 
+// Table loads that should stay in L1: the gathers' cp.async.ca traffic would
+// otherwise evict the small per-launch tables from the L1 left over by shared
+// memory.
+__device__ __forceinline__ int4 ldg_keep(const int4* p) {
+    int4 v;
+    asm("ld.global.nc.L1::evict_last.v4.s32 {%0, %1, %2, %3}, [%4];"
+        : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+        : "l"(p));
+    return v;
+}
+__device__ __forceinline__ int2 ldg_keep(const int2* p) {
+    int2 v;
+    asm("ld.global.nc.L1::evict_last.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ int ldg_keep(const int* p) {
+    int v;
+    asm("ld.global.nc.L1::evict_last.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
     const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
@@ -76,8 +97,8 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_kernel(const __grid_const
         const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(S));
         int i = lane;
         for (; i + 96 < A.nimp; i += 128) {
-            const int2 e0 = __ldg(&A.imports2[i]), e1 = __ldg(&A.imports2[i + 32]);
-            const int2 e2 = __ldg(&A.imports2[i + 64]), e3 = __ldg(&A.imports2[i + 96]);
+            const int2 e0 = ldg_keep(&A.imports2[i]), e1 = ldg_keep(&A.imports2[i + 32]);
+            const int2 e2 = ldg_keep(&A.imports2[i + 64]), e3 = ldg_keep(&A.imports2[i + 96]);
             const double* g0 = sb[e0.x >> 20] + (e0.x & 0xFFFFF);
             const double* g1 = sb[e1.x >> 20] + (e1.x & 0xFFFFF);
             const double* g2 = sb[e2.x >> 20] + (e2.x & 0xFFFFF);
@@ -88,7 +109,7 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_kernel(const __grid_const
             asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sbase + 8u * e3.y), "l"(g3) : "memory");
         }
         for (; i < A.nimp; i += 32) {
-            const int2 e = __ldg(&A.imports2[i]);
+            const int2 e = ldg_keep(&A.imports2[i]);
             const double* g = sb[e.x >> 20] + (e.x & 0xFFFFF);
             asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sbase + 8u * e.y), "l"(g) : "memory");
         }
@@ -109,15 +130,15 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_kernel(const __grid_const
     auto flush = [&](int e0, int e1) {  // record entries [e0, e1) -> HBM (+ ghosts)
         int e = e0 + lane;
         for (; e + 96 < e1; e += 128) {
-            const int o0 = __ldg(&A.exp_off[e]), o1 = __ldg(&A.exp_off[e + 32]);
-            const int o2 = __ldg(&A.exp_off[e + 64]), o3 = __ldg(&A.exp_off[e + 96]);
+            const int o0 = ldg_keep(&A.exp_off[e]), o1 = ldg_keep(&A.exp_off[e + 32]);
+            const int o2 = ldg_keep(&A.exp_off[e + 64]), o3 = ldg_keep(&A.exp_off[e + 96]);
             const double v0 = S[o0], v1 = S[o1], v2 = S[o2], v3 = S[o3];
             dst[e] = v0;
             dst[e + 32] = v1;
             dst[e + 64] = v2;
             dst[e + 96] = v3;
         }
-        for (; e < e1; e += 32) dst[e] = S[__ldg(&A.exp_off[e])];
+        for (; e < e1; e += 32) dst[e] = S[ldg_keep(&A.exp_off[e])];
         if (edge)
             for (int e2 = e0 + lane; e2 < e1; e2 += 32) {
                 const double v = S[__ldg(&A.exp_off[e2])];
