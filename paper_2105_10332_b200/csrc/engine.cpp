@@ -245,6 +245,9 @@ void Solver::finalize_swept() {
             d.d_lev[kd] = dev_upload(d, lv);
             d.d_exp_off[kd] = dev_upload(d, K.exp_off);
             d.d_exp_vs[kd] = dev_upload(d, K.exp_vstride);
+            std::vector<int2> ep;
+            for (const auto& e : K.exp_pairs) ep.push_back(make_int2(e[0], e[1]));
+            d.d_exp_pairs[kd] = dev_upload(d, ep);
             std::vector<int4> ln;
             std::vector<int2> pt;
             for (const auto& e : K.lanes) ln.push_back(make_int4(e[0], e[1], e[2], e[3]));
@@ -307,6 +310,7 @@ void Solver::finalize_swept() {
             a.lev = d.d_lev[L.kind];
             a.exp_off = d.d_exp_off[L.kind];
             a.exp_vs = d.d_exp_vs[L.kind];
+            a.exp_pairs = d.d_exp_pairs[L.kind];
             a.lanes = d.d_lanes[L.kind];
             a.pitch = d.d_pitch[L.kind];
             a.imports = d.d_imp[L.cls];
@@ -361,16 +365,8 @@ void Solver::finalize_swept() {
                 const PlanLevel& Lc = K.at(r);
                 const PlanLevel& Lp = K.at(r - 1);
                 const int w = Lc.comp.w(), h = Lc.comp.h();
-                const int cap = w >= 32 ? 1 : std::max(1, std::min(h, 32 / std::max(1, w)));
-                int splits = 1;
-                for (int dd = cap; dd >= 1; --dd)
-                    if (h % dd == 0) {
-                        splits = dd;
-                        break;
-                    }
-                if (2 * splits < cap) splits = cap;
-                const int rps = (h + splits - 1) / splits;
-                splits = (h + rps - 1) / rps;
+                int splits, rps;
+                lane_split(w, h, &splits, &rps);
                 HeatLevel hl;
                 hl.cx0 = Lc.comp.x0;
                 hl.cy0 = Lc.comp.y0;

@@ -39,6 +39,7 @@ struct DeviceCtx {
     DevLevel* d_lev[K_NKINDS] = {};
     int* d_exp_off[K_NKINDS] = {};
     int* d_exp_vs[K_NKINDS] = {};
+    int2* d_exp_pairs[K_NKINDS] = {};
     int4* d_lanes[K_NKINDS] = {};
     int2* d_pitch[K_NKINDS] = {};
     std::vector<int4*> d_imp, d_init;

@@ -130,25 +130,29 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_kernel(const __grid_const
     auto flush = [&](int e0, int e1) {  // record entries [e0, e1) -> HBM (+ ghosts)
         int e = e0 + lane;
         for (; e + 96 < e1; e += 128) {
-            const int o0 = ldg_keep(&A.exp_off[e]), o1 = ldg_keep(&A.exp_off[e + 32]);
-            const int o2 = ldg_keep(&A.exp_off[e + 64]), o3 = ldg_keep(&A.exp_off[e + 96]);
-            const double v0 = S[o0], v1 = S[o1], v2 = S[o2], v3 = S[o3];
-            dst[e] = v0;
-            dst[e + 32] = v1;
-            dst[e + 64] = v2;
-            dst[e + 96] = v3;
+            const int2 p0 = ldg_keep(&A.exp_pairs[e]), p1 = ldg_keep(&A.exp_pairs[e + 32]);
+            const int2 p2 = ldg_keep(&A.exp_pairs[e + 64]), p3 = ldg_keep(&A.exp_pairs[e + 96]);
+            const double v0 = S[p0.x], v1 = S[p1.x], v2 = S[p2.x], v3 = S[p3.x];
+            dst[p0.y] = v0;
+            dst[p1.y] = v1;
+            dst[p2.y] = v2;
+            dst[p3.y] = v3;
         }
-        for (; e < e1; e += 32) dst[e] = S[ldg_keep(&A.exp_off[e])];
+        for (; e < e1; e += 32) {
+            const int2 p = ldg_keep(&A.exp_pairs[e]);
+            dst[p.y] = S[p.x];
+        }
         if (edge)
             for (int e2 = e0 + lane; e2 < e1; e2 += 32) {
-                const double v = S[__ldg(&A.exp_off[e2])];
+                const int2 p = ldg_keep(&A.exp_pairs[e2]);
+                const double v = S[p.x];
                 for (int ej = -1; ej <= 1; ++ej)
                     for (int ei = -1; ei <= 1; ++ei) {
                         if (ei == 0 && ej == 0) continue;
                         const int tbi = bi - ei * A.pbx, tbj = bj - ej * A.pby;
                         if (tbi < -gh || tbi >= A.pbx + gh || tbj < -gh || tbj >= A.pby + gh) continue;
                         const int tp = wrapi(pj + ej, A.py) * A.px + wrapi(pi + ei, A.px);
-                        A.rec[tp * A.nslots + A.my_slot][((long)(tbj + gh) * A.extw + (tbi + gh)) * A.epad + e2] = v;
+                        A.rec[tp * A.nslots + A.my_slot][((long)(tbj + gh) * A.extw + (tbi + gh)) * A.epad + p.y] = v;
                     }
             }
     };

@@ -39,6 +39,7 @@ struct SweptArgs {
     const DevLevel* lev;     // [nlev - rmin + 1]
     const int* exp_off;      // [nexp]
     const int* exp_vs;       // [nexp]
+    const int2* exp_pairs;   // [nexp] {smem off, record idx}, bank-spread within 32-groups
     const int4* lanes;       // [nlev][32] warp lane map (heat)
     const int2* pitch;       // [nlev] {bbox width at r-1, at r}
     // class tables

@@ -56,7 +56,64 @@ struct RImport {
     }
 };
 
+// 8-byte shared accesses of one warp instruction: wavefronts = per half warp
+// the max number of distinct addresses sharing a bank pair
+int wavefronts(const std::vector<long>& addr) {
+    int wf = 0;
+    for (int h = 0; h < 2; ++h) {
+        std::map<long, std::vector<long>> bank;
+        for (std::size_t l = h * 16; l < std::min<std::size_t>(addr.size(), h * 16 + 16); ++l)
+            if (addr[l] >= 0) {
+                auto& v = bank[((addr[l] % 16) + 16) % 16];
+                if (std::find(v.begin(), v.end(), addr[l]) == v.end()) v.push_back(addr[l]);
+            }
+        int mx = 0;
+        for (auto& kv : bank) mx = std::max<int>(mx, static_cast<int>(kv.second.size()));
+        wf += mx;
+    }
+    return wf;
+}
+
 }  // namespace
+
+void lane_split(int w, int h, int* splits_out, int* rps_out) {
+    const int cap = w >= 32 ? 1 : std::max(1, std::min(h, 32 / std::max(1, w)));
+    int splits = 1;
+    for (int d = cap; d >= 1; --d)
+        if (h % d == 0) {
+            splits = d;
+            break;
+        }
+    if (2 * splits < cap) splits = cap;  // no good divisor: accept a ragged last chunk
+    const int rps = (h + splits - 1) / splits;
+    *splits_out = (h + rps - 1) / rps;
+    *rps_out = rps;
+}
+
+template <class T, class Key>
+void spread_banks(std::vector<T>& v, std::size_t begin, std::size_t end, Key key) {
+    for (std::size_t g = begin; g < end; g += 32) {
+        const std::size_t ge = std::min(end, g + 32);
+        std::vector<T> in(v.begin() + g, v.begin() + ge), out;
+        std::vector<bool> used(in.size(), false);
+        for (int half = 0; half < 2 && out.size() < in.size(); ++half) {
+            bool taken[16] = {false};
+            const std::size_t target = std::min(in.size(), out.size() + 16);
+            for (std::size_t i = 0; i < in.size() && out.size() < target; ++i)  // one per bank pair first
+                if (!used[i] && !taken[((key(in[i]) % 16) + 16) % 16]) {
+                    taken[((key(in[i]) % 16) + 16) % 16] = true;
+                    used[i] = true;
+                    out.push_back(in[i]);
+                }
+            for (std::size_t i = 0; i < in.size() && out.size() < target; ++i)
+                if (!used[i]) {
+                    used[i] = true;
+                    out.push_back(in[i]);
+                }
+        }
+        std::copy(out.begin(), out.end(), v.begin() + g);
+    }
+}
 
 SweptPlan compile_swept_plan(int b, const Equation& eq, long m, long final_level) {
     SweptPlan P;
@@ -252,6 +309,39 @@ SweptPlan compile_swept_plan(int b, const Equation& eq, long m, long final_level
             if (it != box.end()) pl.bbox = it->second;
             pl.off = off;
             pl.pitch = pl.bbox.w();
+            if (eq.problem == SG_HEAT && !pl.bbox.empty()) {
+                // row pitch >= width that makes the lane maps touching this level
+                // (its own writes, level r+1's reads) free of bank conflicts
+                std::vector<std::vector<std::pair<int, int>>> maps;  // lane -> (x, y)
+                for (int rr : {r, r + 1}) {
+                    if (rr < 1 || rr > K.nlev) continue;
+                    const Rect cr = kind_rect(kd, b, n, k, rr);
+                    int sp, rp;
+                    lane_split(cr.w(), cr.h(), &sp, &rp);
+                    std::vector<std::pair<int, int>> m;
+                    for (int l = 0; l < 32; ++l)
+                        if (cr.w() <= 32 && l < cr.w() * sp && cr.y0 + (l / cr.w()) * rp < cr.y1)
+                            m.push_back({cr.x0 + l % cr.w(), cr.y0 + (l / cr.w()) * rp});
+                        else
+                            m.push_back({-1 << 20, 0});
+                    maps.push_back(m);
+                }
+                int best = -1, bestp = pl.bbox.w();
+                for (int cand = pl.bbox.w(); cand < pl.bbox.w() + 16; ++cand) {
+                    int cost = 0;
+                    for (const auto& m : maps) {
+                        std::vector<long> a;
+                        for (const auto& xy : m)
+                            a.push_back(xy.first < -1000 ? -1 : (long)(xy.second - pl.bbox.y0) * cand + (xy.first - pl.bbox.x0));
+                        cost += wavefronts(a);
+                    }
+                    if (best < 0 || cost < best) {
+                        best = cost;
+                        bestp = cand;
+                    }
+                }
+                pl.pitch = bestp;
+            }
             pl.vstride = pl.bbox.h() * pl.pitch;
             if (r >= 1) pl.comp = kind_rect(kd, b, n, k, r);
             off += pl.vstride * P.nvars;
@@ -290,6 +380,9 @@ SweptPlan compile_swept_plan(int b, const Equation& eq, long m, long final_level
             K.exp_vstride.push_back(pl.vstride);
         }
         K.epad = static_cast<int>((K.exp_cells.size() + 3) / 4 * 4);
+        for (std::size_t i = 0; i < K.exp_off.size(); ++i) K.exp_pairs.push_back({K.exp_off[i], static_cast<int>(i)});
+        spread_banks(K.exp_pairs, 0, K.nexp_early, [](const std::array<int, 2>& e) { return e[0]; });
+        spread_banks(K.exp_pairs, K.nexp_early, K.exp_pairs.size(), [](const std::array<int, 2>& e) { return e[0]; });
         // warp lane map: (column, row-chunk) items of each computed rectangle;
         // the row split divides the height exactly when it can, so every
         // active lane runs the same trip count (no divergent row loops)
@@ -298,15 +391,8 @@ SweptPlan compile_swept_plan(int b, const Equation& eq, long m, long final_level
             const PlanLevel& Lp = K.at(r - 1);
             const int w = Lc.comp.w(), h = Lc.comp.h();
             K.pitch.push_back({Lp.pitch, Lc.pitch});
-            const int cap = w >= 32 ? 1 : std::max(1, std::min(h, 32 / std::max(1, w)));
-            int splits = 1;
-            for (int d = cap; d >= 1; --d)
-                if (h % d == 0) {
-                    splits = d;
-                    break;
-                }
-            if (2 * splits < cap) splits = cap;  // no good divisor: accept a ragged last chunk
-            const int rps = (h + splits - 1) / splits;
+            int splits, rps;
+            lane_split(w, h, &splits, &rps);
             for (int l = 0; l < 32; ++l) {
                 std::array<int, 4> e{0, 0, 0, 0};
                 if (w <= 32 && l < w * splits) {
@@ -374,6 +460,7 @@ SweptPlan compile_swept_plan(int b, const Equation& eq, long m, long final_level
         std::sort(T.imports.begin(), T.imports.end(), [](const Import& a, const Import& c) {
             return std::tie(a.seg, a.src) < std::tie(c.seg, c.src);
         });
+        spread_banks(T.imports, 0, T.imports.size(), [](const Import& e) { return e.dst; });
         return T;
     };
     int maxdelta = 0, ghost = 0;

@@ -41,6 +41,10 @@ struct KindLayout {
     // export list: record index i -> (r, x, y) and its smem offset (var 0)
     std::vector<std::array<int, 3>> exp_cells;
     std::vector<int> exp_off, exp_vstride;
+    // the scatter's table: {smem offset, record index}; inside every aligned
+    // group of 32 (one warp instruction) the entries are permuted so the smem
+    // reads hit distinct bank pairs (global coalescing is unchanged)
+    std::vector<std::array<int, 2>> exp_pairs;
     int epad = 0;                 // record length, padded to a multiple of 4
     // storage reuse: levels > split receive no imports and are laid out over
     // the storage of levels < split-S+1; exports of levels <= split (the
@@ -103,6 +107,16 @@ struct SweptPlan {
     long imports_per_kind[K_NKINDS] = {0, 0, 0, 0, 0};
     long updates_per_kind[K_NKINDS] = {0, 0, 0, 0, 0};
 };
+
+// Warp lane map of a w x h rectangle: lanes take (column, row-chunk) items;
+// the row split divides h exactly when it can (uniform trip counts).
+void lane_split(int w, int h, int* splits, int* rps);
+
+// Reorder the entries of every aligned group of 32 so that, within each half
+// warp, the 8-byte shared-memory addresses key(e) fall on distinct bank pairs
+// where possible.
+template <class T, class Key>
+void spread_banks(std::vector<T>& v, std::size_t begin, std::size_t end, Key key);
 
 // m = octahedra; final_level = the level the run must output.
 SweptPlan compile_swept_plan(int b, const Equation& eq, long m, long final_level);
