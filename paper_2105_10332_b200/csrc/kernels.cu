@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(256) std_euler_kernel(const __grid_constant__ 
         }
     };
     int err = 0;
-    euler_rect(tid, T, x0, x1, y0, y1, Q, B, O, ps, fxs, fys, A.c0, A.c1, A.c2, err);
+    euler_rect<true>(tid, T, x0, x1, y0, y1, Q, B, O, ps, fxs, fys, A.c0, A.c1, A.c2, err);
     if (err) *A.err = 1;
 }
 
