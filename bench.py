@@ -350,6 +350,29 @@ def main():
                 s.close()
             eu["swept_over_standard"] = eu["swept"]["value"] / eu["standard"]["value"]
             extra["euler_960_b16"] = eu
+            # the paper's own array sizes, b16, 500 requested steps:
+            # the launch/latency-bound regime the swept rule targets
+            ps = {}
+            for prob in ("heat", "euler"):
+                for nxp in (320, 640, 960):
+                    rates = {}
+                    steps_p = 500
+                    for eng in ("swept", "standard"):
+                        s = sg.Solver(sg.SolverConfig(problem=prob, nx=nxp, block=16, engine=eng, steps=steps_p))
+                        for _ in range(3):
+                            s.reset()
+                            s.solve()
+                        ts = []
+                        for _ in range(args.steps):
+                            s.reset()
+                            ts.append(s.solve())
+                        r = s.fetch().record
+                        s.close()
+                        rates[eng] = r.cell_updates / min(ts)
+                        steps_p = r.actual_steps
+                    ps[f"{prob}_{nxp}"] = {"swept": rates["swept"], "standard": rates["standard"],
+                                           "swept_over_standard": rates["swept"] / rates["standard"]}
+            extra["paper_sizes_b16"] = ps
 
     # ---- CPU baseline: the reference on this host, bounded sample ----------
     cpu = None

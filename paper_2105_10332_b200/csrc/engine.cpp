@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -137,10 +138,12 @@ Solver::Solver(const sg_config& cfg, int rank, int world) : cfg_(cfg), rank_(ran
         ck(cudaSetDevice(d.dev), "cudaSetDevice");
         ck(cudaDeviceSynchronize(), "setup sync");
     }
+    if (const char* v = std::getenv("SG_NO_GRAPH"); v && v[0] == '1') use_graph_ = false;
     setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
 Solver::~Solver() {
+    if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
     for (auto& d : devs_) {
         cudaSetDevice(d.dev);
         cudaStreamSynchronize(d.stream);
@@ -537,81 +540,103 @@ double Solver::solve() {
         writer = std::make_unique<SnapshotWriter>(snap_path_, m);
         writer->append_frame(0, setup_.initial.data());  // level 0 % every == 0
     }
-    if (cfg_.engine == SG_SWEPT) {
-        for (std::size_t li = 0; li < plan_.launches.size(); ++li) {
-            const bool pr = profile && plan_.launches[li].kind == prof_kind_;
-            for (auto& d : devs_) {
-                if (multi) cudaSetDevice(d.dev);
-                if (&d == &d0) prof_begin(pr);
-                ck(launch_swept(prob, d.swept_args[li], d.stream), "swept launch");
-                if (&d == &d0) prof_end(pr);
-                ++launches_;
-            }
-            if (pr) {
-                ++prof_launches_;
-                const Launch& L = plan_.launches[li];
-                const ClassTab& T = plan_.classes[L.cls];
-                const double inst = static_cast<double>(pw_ / cfg_.block) * (ph_ / cfg_.block) *
-                                    devs_[0].parts.size();
-                prof_bytes_ += inst * (T.imports.size() + T.inits.size() + plan_.kinds[L.kind].exp_cells.size()) *
-                               setup_.eq.nvars * 8.0;
-                prof_updates_ += inst * plan_.updates_per_kind[L.kind];
-            }
-            cross_sync();
-            if (writer)
-                for (long l : done_after_[li])
-                    if (l % snap_every_ == 0) snapshot_frame(*writer, l, static_cast<int>(l % frame_ring_));
-        }
-    } else {
-        const Equation& eq = setup_.eq;
-        const int S = eq.substeps;
-        for (long l = 1; l <= final_level_; ++l) {
-            const int phase = static_cast<int>(l % (S + 1));
-            const int stage = static_cast<int>((l - 1) % S);
-            const bool pr = profile;
-            for (auto& d : devs_) {
-                if (multi) cudaSetDevice(d.dev);
-                StdArgs a;
-                std::memset(&a, 0, sizeof a);
-                a.nvars = eq.nvars;
-                a.n = eq.halo;
-                a.pw = pw_;
-                a.ph = ph_;
-                a.px = px_;
-                a.py = py_;
-                a.pitch = pw_ + 2 * eq.halo;
-                a.rows = ph_ + 2 * eq.halo;
-                a.stage = stage;
-                a.ndev_parts = static_cast<int>(d.parts.size());
-                for (std::size_t q = 0; q < d.parts.size(); ++q) a.dev_parts[q] = d.parts[q];
-                a.read1 = d.d_std_r1[phase];
-                a.read2 = l >= 2 ? d.d_std_r2[phase] : d.d_std_r1[phase];
-                a.out = d.d_std_out[phase];
-                if (eq.problem == SG_HEAT) {
-                    a.c0 = setup_.heat_fx;
-                    a.c1 = setup_.heat_fy;
-                } else {
-                    a.c0 = setup_.gamma;
-                    a.c1 = stage == 0 ? setup_.cx_pred : setup_.cx_corr;
-                    a.c2 = stage == 0 ? setup_.cy_pred : setup_.cy_corr;
+    auto enqueue = [&]() {
+        if (cfg_.engine == SG_SWEPT) {
+            for (std::size_t li = 0; li < plan_.launches.size(); ++li) {
+                const bool pr = profile && plan_.launches[li].kind == prof_kind_;
+                for (auto& d : devs_) {
+                    if (multi) cudaSetDevice(d.dev);
+                    if (&d == &d0) prof_begin(pr);
+                    ck(launch_swept(prob, d.swept_args[li], d.stream), "swept launch");
+                    if (&d == &d0) prof_end(pr);
+                    ++launches_;
                 }
-                a.err = d.d_err;
-                if (&d == &d0) prof_begin(pr);
-                ck(launch_std(eq.problem, a, d.stream), "std launch");
-                if (&d == &d0) prof_end(pr);
-                ++launches_;
+                if (pr) {
+                    ++prof_launches_;
+                    const Launch& L = plan_.launches[li];
+                    const ClassTab& T = plan_.classes[L.cls];
+                    const double inst = static_cast<double>(pw_ / cfg_.block) * (ph_ / cfg_.block) *
+                                        devs_[0].parts.size();
+                    prof_bytes_ += inst * (T.imports.size() + T.inits.size() + plan_.kinds[L.kind].exp_cells.size()) *
+                                   setup_.eq.nvars * 8.0;
+                    prof_updates_ += inst * plan_.updates_per_kind[L.kind];
+                }
+                cross_sync();
+                if (writer)
+                    for (long l : done_after_[li])
+                        if (l % snap_every_ == 0) snapshot_frame(*writer, l, static_cast<int>(l % frame_ring_));
             }
-            if (pr) {
-                ++prof_launches_;
-                const double cells = static_cast<double>(pw_) * ph_ * devs_[0].parts.size();
-                // heat: read 8 + write 8; euler: predictor 64, corrector 96
-                const double bpu = eq.problem == SG_HEAT ? 16.0 : (stage == 0 ? 64.0 : 96.0);
-                prof_bytes_ += cells * bpu;
-                prof_updates_ += cells;
+        } else {
+            const Equation& eq = setup_.eq;
+            const int S = eq.substeps;
+            for (long l = 1; l <= final_level_; ++l) {
+                const int phase = static_cast<int>(l % (S + 1));
+                const int stage = static_cast<int>((l - 1) % S);
+                const bool pr = profile;
+                for (auto& d : devs_) {
+                    if (multi) cudaSetDevice(d.dev);
+                    StdArgs a;
+                    std::memset(&a, 0, sizeof a);
+                    a.nvars = eq.nvars;
+                    a.n = eq.halo;
+                    a.pw = pw_;
+                    a.ph = ph_;
+                    a.px = px_;
+                    a.py = py_;
+                    a.pitch = pw_ + 2 * eq.halo;
+                    a.rows = ph_ + 2 * eq.halo;
+                    a.stage = stage;
+                    a.ndev_parts = static_cast<int>(d.parts.size());
+                    for (std::size_t q = 0; q < d.parts.size(); ++q) a.dev_parts[q] = d.parts[q];
+                    a.read1 = d.d_std_r1[phase];
+                    a.read2 = l >= 2 ? d.d_std_r2[phase] : d.d_std_r1[phase];
+                    a.out = d.d_std_out[phase];
+                    if (eq.problem == SG_HEAT) {
+                        a.c0 = setup_.heat_fx;
+                        a.c1 = setup_.heat_fy;
+                    } else {
+                        a.c0 = setup_.gamma;
+                        a.c1 = stage == 0 ? setup_.cx_pred : setup_.cx_corr;
+                        a.c2 = stage == 0 ? setup_.cy_pred : setup_.cy_corr;
+                    }
+                    a.err = d.d_err;
+                    if (&d == &d0) prof_begin(pr);
+                    ck(launch_std(eq.problem, a, d.stream), "std launch");
+                    if (&d == &d0) prof_end(pr);
+                    ++launches_;
+                }
+                if (pr) {
+                    ++prof_launches_;
+                    const double cells = static_cast<double>(pw_) * ph_ * devs_[0].parts.size();
+                    // heat: read 8 + write 8; euler: predictor 64, corrector 96
+                    const double bpu = eq.problem == SG_HEAT ? 16.0 : (stage == 0 ? 64.0 : 96.0);
+                    prof_bytes_ += cells * bpu;
+                    prof_updates_ += cells;
+                }
+                cross_sync();
+                if (writer && l % snap_every_ == 0) snapshot_frame(*writer, l, static_cast<int>(l % (S + 1)));
             }
-            cross_sync();
-            if (writer && l % snap_every_ == 0) snapshot_frame(*writer, l, static_cast<int>(l % (S + 1)));
         }
+    };
+    // Single-GPU solves without snapshots/profiling are replayed from a CUDA
+    // graph captured on the first solve: every launch of the solve (up to
+    // ~4300 phase launches at 10k steps) goes to the GPU in one call.
+    const bool graphable = !multi && !dist() && !writer && !profile && use_graph_;
+    if (graphable) {
+        DeviceCtx& d = devs_[0];
+        if (!graph_exec_) {
+            cudaGraph_t g = nullptr;
+            ck(cudaStreamBeginCapture(d.stream, cudaStreamCaptureModeThreadLocal), "capture");
+            enqueue();
+            ck(cudaStreamEndCapture(d.stream, &g), "capture");
+            ck(cudaGraphInstantiate(&graph_exec_, g, 0), "graph instantiate");
+            cudaGraphDestroy(g);
+            graph_launches_ = launches_;
+        }
+        launches_ = graph_launches_;
+        ck(cudaGraphLaunch(graph_exec_, d.stream), "graph launch");
+    } else {
+        enqueue();
     }
     double worst = 0.0;
     for (auto& d : devs_) {

@@ -70,6 +70,7 @@ class Solver {
     const Setup& setup() const { return setup_; }
     double setup_seconds = 0.0;
     bool profile = false;
+    bool use_graph_ = true;   // SG_NO_GRAPH=1 disables CUDA graph replay
 
     // distributed (one process per GPU): export this rank's buffers as CUDA
     // IPC handles, then map every other rank's and build the kernel tables
@@ -104,6 +105,8 @@ class Solver {
     unsigned long long** d_peer_flags_ = nullptr;
     unsigned long long epoch_ = 0;
     std::vector<void*> ipc_open_;
+    cudaGraphExec_t graph_exec_ = nullptr;
+    long graph_launches_ = 0;
     // snapshots (SWPT2D, snapshot.cpp of the reference)
     std::string snap_path_;
     long snap_every_ = 1;
