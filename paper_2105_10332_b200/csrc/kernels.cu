@@ -20,6 +20,8 @@
 //  dist_barrier_kernel: cross-process launch ordering (one process per GPU).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "kernels.cuh"
 #include "physics.cuh"
 
@@ -232,7 +234,8 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_kernel(const __grid_const
 // the heat kernel (4 variables per record entry), then every level of the
 // phase runs through euler_rect on shared memory (pressures, shared x/y
 // interface fluxes, update), then the record is scattered.
-__global__ void __launch_bounds__(128) swept_euler_kernel(const __grid_constant__ SweptArgs A) {
+template <int MINB>
+__global__ void __launch_bounds__(128, MINB) swept_euler_kernel(const __grid_constant__ SweptArgs A) {
     extern __shared__ double S[];
     __shared__ const double* sb[kMaxSegs];
     const int tid = threadIdx.x, T = 128;
@@ -350,8 +353,8 @@ __global__ void __launch_bounds__(128) swept_euler_kernel(const __grid_constant_
 // radius-2 neighbourhood of the tile is staged in shared memory, then
 // euler_rect (shared interface fluxes); boundary cells are pushed into the
 // neighbouring partitions' ghost frames.
-template <int TX, int TY>
-__global__ void __launch_bounds__(256) std_euler_kernel(const __grid_constant__ StdArgs A) {
+template <int TX, int TY, int MINB>
+__global__ void __launch_bounds__(256, MINB) std_euler_kernel(const __grid_constant__ StdArgs A) {
     constexpr int QW = TX + 4, QH = TY + 4;
     __shared__ double q[4][QH][QW];
     __shared__ double ps[QH * QW];
@@ -607,10 +610,13 @@ cudaError_t launch_swept(int problem, const SweptArgs& a, cudaStream_t s) {
     }
     {
         const size_t smem = static_cast<size_t>(a.smem_doubles + a.ps_doubles + 2 * a.fx_doubles) * sizeof(double);
-        if (smem > 48 * 1024)
-            cudaFuncSetAttribute(swept_euler_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        // 7 resident CTAs (<= 72 registers): occupancy hides the FP64
+        // dependency chains and the per-level barriers (1.09e10 vs 8.5e9
+        // updates/s at 112 registers, Euler 960^2 b16)
+        auto kern = swept_euler_kernel<7>;
+        if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         dim3 grid(ninst, a.ndev_parts);
-        swept_euler_kernel<<<grid, 128, smem, s>>>(a);
+        kern<<<grid, 128, smem, s>>>(a);
         return cudaGetLastError();
     }
 }
@@ -626,7 +632,8 @@ cudaError_t launch_std(int problem, const StdArgs& a, cudaStream_t s) {
         // 32 x 7: the fused flux step has 7*33 + 8*32 = 487 items = two rounds of 256
         constexpr int TX = 32, TY = 7;
         dim3 grid((a.pw + TX - 1) / TX, (a.ph + TY - 1) / TY, a.ndev_parts);
-        std_euler_kernel<TX, TY><<<grid, 256, 0, s>>>(a);
+        // 4 resident CTAs (64 registers, no spills): 1.58e10 vs 1.01e10 at 96
+        std_euler_kernel<TX, TY, 4><<<grid, 256, 0, s>>>(a);
         return cudaGetLastError();
     }
     dim3 block(32, 8);
