@@ -1,0 +1,142 @@
+// Closed-form geometry of the column-register heat phase kernels, shared by
+// the plan compiler (host) and the kernels (device) so both agree on where
+// every imported cell lands in shared memory and where every exported cell
+// sits in an instance's record.
+//
+// Column mode (heat, n = 1, S = 1, block B in {8, 16, 32}): B lanes own one
+// phase instance, lane c = instance column c, and each lane holds its
+// column's cells of the current level in registers, rows [ylo, ylo + B).
+// Every kind's cells (computed and read) fit that B x B window:
+//   UpPyramid / Octahedron / DownPyramid rows [0, B), YBridge / XBridge rows
+//   [B/2, 3B/2); columns [0, B) for all (phase_region, geometry.cpp:93-115).
+//
+// Level r of a kind reads level r-1 on the cross Read(R_r) = R_r grown by one
+// in x (rows of R_r) and one in y (columns of R_r).  What the instance did not
+// compute itself at r-1 (R_{r-1}) is imported:
+//     imports(r) = Read(R_r) \ R_{r-1}            (R_0 = empty)
+// and a cell of R_r is exported iff another instance reads it at r+1, i.e.
+// unless it and its four neighbours all lie in R_{r+1}:
+//     exports(r) = R_r \ interior(R_{r+1})        (R_{nlev+1} = empty)
+// Both sets are, row by row, a column interval minus a column hole; they are
+// enumerated level by level, row by row, column by column.  The plan compiler
+// checks them against its schedule replay (plan.cpp) before using them.
+#pragma once
+
+#if defined(__CUDACC__)
+#define SG_HD __host__ __device__
+#else
+#define SG_HD
+#endif
+
+namespace sg {
+namespace col {
+
+// Kind ids (= sg::Kind, checked by a static_assert in plan.cpp)
+constexpr int UP = 0, YB = 1, XB = 2, OCT = 3, DOWN = 4;
+
+struct CRect {
+    int x0, x1, y0, y1;
+};
+
+SG_HD constexpr int nlev(int kind, int B) { return kind == OCT ? 2 * (B / 2 - 1) : B / 2 - 1; }
+SG_HD constexpr int ylo(int kind, int B) { return (kind == YB || kind == XB) ? B / 2 : 0; }
+
+// phase_region (geometry.cpp:93-115) for n = 1, k = B/2 - 1; empty outside 1..nlev
+SG_HD constexpr CRect rect(int kind, int B, int r) {
+    const int k = B / 2 - 1;
+    if (r < 1 || r > nlev(kind, B)) return CRect{0, 0, 0, 0};
+    switch (kind) {
+        case UP: return CRect{r, B - r, r, B - r};
+        case YB: return CRect{r, B - r, B - r, B + r};
+        case XB: return CRect{B / 2 - r, B / 2 + r, B / 2 + r, 3 * B / 2 - r};
+        case DOWN: return CRect{B / 2 - r, B / 2 + r, B / 2 - r, B / 2 + r};
+        default: {
+            if (r <= k) return CRect{B / 2 - r, B / 2 + r, B / 2 - r, B / 2 + r};
+            const int w = B - 2 * (r - k);
+            return CRect{B / 2 - w / 2, B / 2 + w / 2, B / 2 - w / 2, B / 2 + w / 2};
+        }
+    }
+}
+SG_HD constexpr bool empty(CRect q) { return q.x1 <= q.x0 || q.y1 <= q.y0; }
+
+// one row of a cell set: columns [a, b) minus [hp, hq)
+struct RowSet {
+    int a, b, hp, hq;
+    SG_HD constexpr int count() const { return b > a ? (b - a) - (hq - hp) : 0; }
+    SG_HD constexpr bool has(int x) const { return x >= a && x < b && !(x >= hp && x < hq); }
+    // rank of column x among the row's columns
+    SG_HD constexpr int rank(int x) const { return x - a - (x >= hq ? hq - hp : 0); }
+};
+
+SG_HD constexpr RowSet make_row(int a, int b, int hp, int hq) {
+    if (b <= a) return RowSet{0, 0, 0, 0};
+    if (hp < a) hp = a;
+    if (hq > b) hq = b;
+    if (hq <= hp) hp = hq = b;  // no hole
+    return RowSet{a, b, hp, hq};
+}
+
+// imported columns of row y at level r-1 (read by level r)
+SG_HD constexpr RowSet imp_row(int kind, int B, int r, int y) {
+    const CRect q = rect(kind, B, r);
+    if (empty(q)) return RowSet{0, 0, 0, 0};
+    int a = 0, b = 0;
+    if (y >= q.y0 && y < q.y1) {
+        a = q.x0 - 1;
+        b = q.x1 + 1;
+    } else if (y == q.y0 - 1 || y == q.y1) {
+        a = q.x0;
+        b = q.x1;
+    } else {
+        return RowSet{0, 0, 0, 0};
+    }
+    const CRect p = rect(kind, B, r - 1);
+    if (!empty(p) && y >= p.y0 && y < p.y1) return make_row(a, b, p.x0, p.x1);
+    return make_row(a, b, b, b);
+}
+
+// exported columns of row y at level r
+SG_HD constexpr RowSet exp_row(int kind, int B, int r, int y) {
+    if (kind == DOWN) return RowSet{0, 0, 0, 0};  // the last phase: output only
+    const CRect q = rect(kind, B, r);
+    if (empty(q) || y < q.y0 || y >= q.y1) return RowSet{0, 0, 0, 0};
+    const CRect nq = rect(kind, B, r + 1);
+    if (!empty(nq) && y >= nq.y0 + 1 && y < nq.y1 - 1) return make_row(q.x0, q.x1, nq.x0 + 1, nq.x1 - 1);
+    return make_row(q.x0, q.x1, q.x1, q.x1);
+}
+
+// slot of (r, row y) = level base + row base; rows y in [ylo, ylo + B)
+SG_HD constexpr int imp_base(int kind, int B, int r, int y) {
+    int s = 0;
+    for (int rr = 1; rr < r; ++rr)
+        for (int yy = ylo(kind, B); yy < ylo(kind, B) + B; ++yy) s += imp_row(kind, B, rr, yy).count();
+    for (int yy = ylo(kind, B); yy < y; ++yy) s += imp_row(kind, B, r, yy).count();
+    return s;
+}
+SG_HD constexpr int exp_base(int kind, int B, int r, int y) {
+    int s = 0;
+    for (int rr = 1; rr < r; ++rr)
+        for (int yy = ylo(kind, B); yy < ylo(kind, B) + B; ++yy) s += exp_row(kind, B, rr, yy).count();
+    for (int yy = ylo(kind, B); yy < y; ++yy) s += exp_row(kind, B, r, yy).count();
+    return s;
+}
+SG_HD constexpr int imp_total(int kind, int B) { return imp_base(kind, B, nlev(kind, B) + 1, ylo(kind, B)); }
+SG_HD constexpr int exp_total(int kind, int B) { return exp_base(kind, B, nlev(kind, B) + 1, ylo(kind, B)); }
+
+// slot of an imported cell at level r-1 (column x, row y), -1 if not an import
+SG_HD constexpr int imp_slot(int kind, int B, int r, int x, int y) {
+    if (y < ylo(kind, B) || y >= ylo(kind, B) + B) return -1;
+    const RowSet s = imp_row(kind, B, r, y);
+    return s.has(x) ? imp_base(kind, B, r, y) + s.rank(x) : -1;
+}
+// record index of an exported cell at level r, -1 if not exported
+SG_HD constexpr int exp_slot(int kind, int B, int r, int x, int y) {
+    if (y < ylo(kind, B) || y >= ylo(kind, B) + B) return -1;
+    const RowSet s = exp_row(kind, B, r, y);
+    return s.has(x) ? exp_base(kind, B, r, y) + s.rank(x) : -1;
+}
+
+SG_HD constexpr bool supported(int B) { return B == 8 || B == 16 || B == 32; }
+
+}  // namespace col
+}  // namespace sg

@@ -332,6 +332,8 @@ void Solver::finalize_swept() {
             a.stage0 = L.stage0;
             a.r_out = L.r_out;
             a.my_slot = L.slot < 0 ? 0 : L.slot;
+            a.kind = L.kind;
+            a.colB = P.colB;
             a.b = b;
             a.nx = setup_.nx;
             a.ny = setup_.ny;
@@ -364,6 +366,11 @@ void Solver::finalize_swept() {
             a.snap_every = frame_ring_ > 0 ? static_cast<int>(snap_every_) : 0;
             a.frame_ring = std::max(1, frame_ring_);
             a.lo = L.lo;
+            a.out_mask = L.r_out > 0 ? 1ull << L.r_out : 0ull;
+            a.snap_mask = 0;
+            if (a.snap_every > 0)
+                for (int r = 1; r <= K.nlev; ++r)
+                    if ((L.lo + r - 1) % a.snap_every == 0) a.snap_mask |= 1ull << r;
             for (int r = 1; r <= K.nlev; ++r) {  // heat lane map: (column, row-chunk) items of a warp
                 const PlanLevel& Lc = K.at(r);
                 const PlanLevel& Lp = K.at(r - 1);

@@ -21,7 +21,10 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <type_traits>
+#include <utility>
 
+#include "colgeom.hpp"
 #include "kernels.cuh"
 #include "physics.cuh"
 
@@ -228,6 +231,179 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_kernel(const __grid_const
     }
     // ---- 3. scatter the rest of the record
     if (A.nexp > A.nexp_early) flush(A.nexp_early, A.nexp);
+}
+
+// Compile-time loop: f(std::integral_constant<int, I>) for I = 0..N-1.
+template <class F, int... I>
+__device__ __forceinline__ void sfor_impl(F&& f, std::integer_sequence<int, I...>) {
+    (f(std::integral_constant<int, I>{}), ...);
+}
+template <int N, class F>
+__device__ __forceinline__ void sfor(F&& f) {
+    sfor_impl(f, std::make_integer_sequence<int, N>{});
+}
+
+// Writes rows [i0, i1) of one column (stash[i] = window row ylo + i) of an
+// instance to the owning partitions' output plane and/or snapshot frame.
+// x = the column's x relative to the partition origin, y0 = the window's
+// origin row relative to it (both may wrap).
+__device__ __noinline__ void put_column(const SweptArgs& A, const double* stash, int c, int i0, int i1, int ylo,
+                                        int pi, int pj, int x, int y0, long lev, bool out, bool snap) {
+    const long pl = (long)A.pw * A.ph;
+    const int gx = wrapi(pi * A.pw + x, A.nx);
+    const int opi = gx / A.pw;
+    for (int i = i0; i < i1; ++i) {
+        const int gy = wrapi(pj * A.ph + y0 + ylo + i, A.ny);
+        const int opj = gy / A.ph;
+        const long o = (long)(gy - opj * A.ph) * A.pw + (gx - opi * A.pw);
+        if (out) A.out_planes[opj * A.px + opi][o] = stash[i];
+        if (snap) A.frames[opj * A.px + opi][(lev % A.frame_ring) * pl + o] = stash[i];
+    }
+    (void)c;
+}
+
+// Heat phase kernel, column-register form (block B in {8, 16, 32}, geometry
+// in colgeom.hpp).  B lanes own one phase instance (32/B instances per warp,
+// 4 warps per CTA); lane c holds column c of the instance's B x B window in
+// registers, v[i] = row ylo + i of the current level.  Per level r (all
+// geometry is compile-time, levels and rows fully unrolled):
+//   1. imports: the cells of level r-1 this instance did not compute come
+//      from shared memory, where the gather landed them (one predicated LDS
+//      per row; lanes whose cells are imports take them);
+//   2. update rows [y0, y1) of R_r in place: north/south/centre are the
+//      lane's own registers, east/west come from lanes c+1 / c-1 by warp
+//      shuffle (heat_point, physics.hpp:57-63; no FMA);
+//   3. exports: the cells of R_r that other instances read go straight from
+//      registers into this instance's record (contiguous per row).
+// Lanes outside R_r compute too (SIMT); their rows are never read before an
+// import overwrites them.  Nothing but the imports touches shared memory.
+template <int B, int KIND>
+__global__ void __launch_bounds__(128) swept_heat_col_kernel(const __grid_constant__ SweptArgs A) {
+    constexpr int IPW = 32 / B;
+    constexpr int NL = col::nlev(KIND, B);
+    constexpr int YLO = col::ylo(KIND, B);
+    extern __shared__ double sm[];
+    __shared__ const double* segbase[4 * IPW][kMaxSegs];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sub = lane / B, c = lane % B;
+    const int slot_in_cta = warp * IPW + sub;
+    const int ninst = A.pbx * A.pby;
+    const int inst = blockIdx.x * (4 * IPW) + slot_in_cta;
+    const bool live = inst < ninst;
+    const int part = A.dev_parts[blockIdx.y];
+    const int pi = part % A.px, pj = part / A.px;
+    const int bi = live ? inst % A.pbx : 0, bj = live ? inst / A.pbx : 0;
+    const int half = A.frame * (B / 2);
+    double* S = sm + slot_in_cta * A.smem_doubles;
+    const double** sb = segbase[slot_in_cta];
+
+    // ---- gather the imports (records of earlier phases, initial plane)
+    if (live)
+        for (int s = c; s < A.nsegs; s += B) {
+            const DevSeg sg = A.segs[s];
+            const long ext = (long)(bj + sg.dj + A.ghost) * A.extw + (bi + sg.di + A.ghost);
+            sb[s] = A.rec[part * A.nslots + sg.slot] + ext * sg.epad;
+        }
+    __syncwarp();
+    if (live) {
+        int i = c;
+        for (; i + 3 * B < A.nimp; i += 4 * B) {
+            const int2 e0 = ldg_keep(&A.imports2[i]), e1 = ldg_keep(&A.imports2[i + B]);
+            const int2 e2 = ldg_keep(&A.imports2[i + 2 * B]), e3 = ldg_keep(&A.imports2[i + 3 * B]);
+            cp_async8(S + e0.y, sb[e0.x >> 20] + (e0.x & 0xFFFFF));
+            cp_async8(S + e1.y, sb[e1.x >> 20] + (e1.x & 0xFFFFF));
+            cp_async8(S + e2.y, sb[e2.x >> 20] + (e2.x & 0xFFFFF));
+            cp_async8(S + e3.y, sb[e3.x >> 20] + (e3.x & 0xFFFFF));
+        }
+        for (; i < A.nimp; i += B) {
+            const int2 e = ldg_keep(&A.imports2[i]);
+            cp_async8(S + e.y, sb[e.x >> 20] + (e.x & 0xFFFFF));
+        }
+        for (int j = c; j < A.ninit; j += B) {
+            const int4 im = __ldg(&A.inits[j]);
+            const int gx = wrapi(pi * A.pw + bi * B - half + im.x, A.nx);
+            const int gy = wrapi(pj * A.ph + bj * B - half + im.y, A.ny);
+            const int opi = gx / A.pw, opj = gy / A.ph;
+            S[im.z] = A.init_planes[opj * A.px + opi][(long)(gy - opj * A.ph) * A.pw + (gx - opi * A.pw)];
+        }
+    }
+    cp_async_wait_all();
+    __syncwarp();
+
+    const int gh = A.ghost;
+    double* dst = A.rec[part * A.nslots + A.my_slot] + ((long)(bj + gh) * A.extw + (bi + gh)) * A.epad;
+    const double fx = A.c0, fy = A.c1;
+    // output stash (only allocated by launches that write the output level or snapshots)
+    double* stash = sm + 4 * IPW * A.smem_doubles + (slot_in_cta * B + c) * B;
+    double v[B];
+#pragma unroll
+    for (int i = 0; i < B; ++i) v[i] = 0.0;
+
+    sfor<NL>([&](auto RI) {
+        constexpr int r = decltype(RI)::value + 1;
+        constexpr col::CRect q = col::rect(KIND, B, r);
+        // 1. imports of level r-1
+        sfor<B>([&](auto YI) {
+            constexpr int j = decltype(YI)::value;
+            constexpr col::RowSet is = col::imp_row(KIND, B, r, YLO + j);
+            if constexpr (is.count() > 0) {
+                constexpr int base = col::imp_base(KIND, B, r, YLO + j);
+                if (is.has(c)) v[j] = S[base + is.rank(c)];
+            }
+        });
+        // 2. rows [y0, y1) of R_r, in place (prev = the old value of the row below)
+        double prev = v[q.y0 - 1 - YLO];
+        sfor<B>([&](auto YI) {
+            constexpr int j = decltype(YI)::value;
+            constexpr col::CRect qr = col::rect(KIND, B, r);
+            if constexpr (YLO + j >= qr.y0 && YLO + j < qr.y1) {
+                const double cur = v[j];
+                const double e = __shfl_down_sync(0xffffffffu, cur, 1);
+                const double w = __shfl_up_sync(0xffffffffu, cur, 1);
+                const double nv = heat_update(cur, e, w, v[j + 1], prev, fx, fy);
+                prev = cur;
+                v[j] = nv;
+            }
+        });
+        // 3. exports of level r
+        if (live)
+            sfor<B>([&](auto YI) {
+                constexpr int j = decltype(YI)::value;
+                constexpr col::RowSet es = col::exp_row(KIND, B, r, YLO + j);
+                if constexpr (es.count() > 0) {
+                    constexpr int base = col::exp_base(KIND, B, r, YLO + j);
+                    if (es.has(c)) dst[base + es.rank(c)] = v[j];
+                }
+            });
+        // output level / snapshot (rare): the lane's column goes through its
+        // shared-memory stash to a non-inlined writer (keeps the unrolled
+        // level code small)
+        if (((A.out_mask | A.snap_mask) >> r) & 1ull) {
+#pragma unroll
+            for (int i = 0; i < B; ++i) stash[i] = v[i];
+            if (live && c >= q.x0 && c < q.x1)
+                put_column(A, stash, c, q.y0 - YLO, q.y1 - YLO, YLO, pi, pj, bi * B - half + c, bj * B - half,
+                           A.lo + r - 1, (A.out_mask >> r) & 1ull, (A.snap_mask >> r) & 1ull);
+        }
+    });
+
+    // ---- partition-edge instances: copy the record into the neighbours' ghost rings
+    const bool edge = bi < gh || bi >= A.pbx - gh || bj < gh || bj >= A.pby - gh;
+    if (edge && live && A.nexp > 0) {
+        if constexpr (B == 32) __syncwarp();
+        else __syncwarp(((1u << B) - 1u) << (sub * B));
+        for (int e = c; e < A.nexp; e += B) {
+            const double val = __ldcg(dst + e);
+            for (int ej = -1; ej <= 1; ++ej)
+                for (int ei = -1; ei <= 1; ++ei) {
+                    if (ei == 0 && ej == 0) continue;
+                    const int tbi = bi - ei * A.pbx, tbj = bj - ej * A.pby;
+                    if (tbi < -gh || tbi >= A.pbx + gh || tbj < -gh || tbj >= A.pby + gh) continue;
+                    const int tp = wrapi(pj + ej, A.py) * A.px + wrapi(pi + ei, A.px);
+                    A.rec[tp * A.nslots + A.my_slot][((long)(tbj + gh) * A.extw + (tbi + gh)) * A.epad + e] = val;
+                }
+        }
+    }
 }
 
 // Euler phase kernel: one CTA (128 threads) per block instance.  Gather as
@@ -593,8 +769,32 @@ cudaError_t launch_dist_barrier(unsigned long long* const* peer_flags, unsigned 
     return cudaGetLastError();
 }
 
+template <int B>
+cudaError_t launch_heat_col(const SweptArgs& a, cudaStream_t s) {
+    constexpr int IPC = 4 * (32 / B);  // instances per CTA
+    const bool stash = (a.out_mask | a.snap_mask) != 0ull;
+    const size_t smem = static_cast<size_t>(IPC) * (a.smem_doubles + (stash ? B * B : 0)) * sizeof(double);
+    const int ninst = a.pbx * a.pby;
+    dim3 grid((ninst + IPC - 1) / IPC, a.ndev_parts);
+    auto go = [&](auto kern) {
+        if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<grid, 128, smem, s>>>(a);
+        return cudaGetLastError();
+    };
+    switch (a.kind) {
+        case col::UP: return go(swept_heat_col_kernel<B, col::UP>);
+        case col::YB: return go(swept_heat_col_kernel<B, col::YB>);
+        case col::XB: return go(swept_heat_col_kernel<B, col::XB>);
+        case col::OCT: return go(swept_heat_col_kernel<B, col::OCT>);
+        default: return go(swept_heat_col_kernel<B, col::DOWN>);
+    }
+}
+
 cudaError_t launch_swept(int problem, const SweptArgs& a, cudaStream_t s) {
     const int ninst = a.pbx * a.pby;
+    if (problem == 0 && a.colB == 16) return launch_heat_col<16>(a, s);
+    if (problem == 0 && a.colB == 8) return launch_heat_col<8>(a, s);
+    if (problem == 0 && a.colB == 32) return launch_heat_col<32>(a, s);
     if (problem == 0) {
         const size_t per_inst = static_cast<size_t>(a.smem_doubles) * sizeof(double);
         auto go = [&](auto kern, int wpc) {

@@ -52,6 +52,10 @@ struct SweptArgs {
     int nsegs;
     // launch
     int frame, stage0, r_out, my_slot;
+    int kind;                        // phase kind (sg::Kind)
+    int colB;                        // heat: column-register kernels for block colB (0 = generic)
+    unsigned long long out_mask;     // bit r: relative level r is the output level
+    unsigned long long snap_mask;    // bit r: relative level r is a snapshot level
     // geometry
     int b, nx, ny, pw, ph, pbx, pby, px, py, ghost, extw, nslots;
     int ndev_parts;

@@ -3,12 +3,20 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <set>
 #include <map>
 #include <sstream>
 #include <tuple>
 #include <unordered_map>
 
+#include "colgeom.hpp"
+
 namespace sg {
+
+static_assert(col::UP == K_UP && col::YB == K_YB && col::XB == K_XB && col::OCT == K_OCT && col::DOWN == K_DOWN,
+              "colgeom kind ids");
 
 namespace {
 
@@ -126,6 +134,11 @@ SweptPlan compile_swept_plan(int b, const Equation& eq, long m, long final_level
     P.flat = static_cast<long>(P.k) * (m + 1);
     P.final_level = final_level;
     const int n = P.n, k = P.k, S = P.S;
+    {
+        const char* env = std::getenv("SG_HEAT_KERNEL");
+        const bool generic = env && std::strcmp(env, "generic") == 0;
+        if (eq.problem == SG_HEAT && n == 1 && S == 1 && col::supported(b) && !generic) P.colB = b;
+    }
     if (final_level < 1 || final_level > P.flat) fail(SG_ELOGIC, "plan: final level outside the schedule");
 
     const long mr = (m <= MAXR) ? m : (8 + (m % 2));
@@ -414,6 +427,41 @@ SweptPlan compile_swept_plan(int b, const Equation& eq, long m, long final_level
         for (int r = 1; r <= K.nlev; ++r) upd += kind_rect(kd, b, n, k, r).area();
         P.updates_per_kind[kd] = upd;
     }
+    if (P.colB) {
+        // column-register kernels: closed-form export order and import slots
+        // (colgeom.hpp); the replayed export set must be covered
+        P.max_epad = 0;
+        for (int kd = 0; kd < K_NKINDS; ++kd) {
+            KindLayout& K = P.kinds[kd];
+            std::set<std::array<int, 3>> formula;
+            K.exp_cells.clear();
+            K.exp_off.clear();
+            K.exp_vstride.clear();
+            K.exp_pairs.clear();
+            for (int r = 1; r <= K.nlev; ++r)
+                for (int y = col::ylo(kd, b); y < col::ylo(kd, b) + b; ++y)
+                    for (int x = 0; x < b; ++x)
+                        if (col::exp_row(kd, b, r, y).has(x)) {
+                            if (col::exp_slot(kd, b, r, x, y) != static_cast<int>(K.exp_cells.size()))
+                                fail(SG_ELOGIC, "plan: column export order");
+                            formula.insert({r, x, y});
+                            K.exp_cells.push_back({r, x, y});
+                            K.exp_off.push_back(0);
+                            K.exp_vstride.push_back(0);
+                            K.exp_pairs.push_back({0, static_cast<int>(K.exp_pairs.size())});
+                        }
+            if (static_cast<int>(K.exp_cells.size()) != col::exp_total(kd, b))
+                fail(SG_ELOGIC, "plan: column export count");
+            for (auto& kv : exp_mask[kd])
+                if (!formula.count(kv.first)) fail(SG_ELOGIC, "plan: column exports miss a replayed read");
+            P.overexport += static_cast<long>(formula.size() - exp_mask[kd].size());
+            K.epad = static_cast<int>((K.exp_cells.size() + 3) / 4 * 4);
+            K.smem_doubles = std::max(1, col::imp_total(kd, b));
+            K.split = K.nlev;
+            K.nexp_early = 0;
+            P.max_epad = std::max(P.max_epad, K.epad);
+        }
+    }
     std::map<std::array<int, 3>, int> exp_index[K_NKINDS];
     for (int kd = 0; kd < K_NKINDS; ++kd)
         for (std::size_t i = 0; i < P.kinds[kd].exp_cells.size(); ++i) {
@@ -430,7 +478,11 @@ SweptPlan compile_swept_plan(int b, const Equation& eq, long m, long final_level
         std::map<std::tuple<int, int, int, int>, int> seg_id;
         for (const RImport& im : rep_imports[L]) {
             const PlanLevel& pl = K.at(im.r);
-            const int dst = pl.off + (im.qy - pl.bbox.y0) * pl.pitch + (im.qx - pl.bbox.x0);
+            int dst = pl.off + (im.qy - pl.bbox.y0) * pl.pitch + (im.qx - pl.bbox.x0);
+            if (P.colB) {  // level im.r is read by level im.r + 1
+                dst = col::imp_slot(T.kind, b, im.r + 1, im.qx, im.qy);
+                if (dst < 0) fail(SG_ELOGIC, "plan: import outside the column layout");
+            }
             if (im.delta == 0) {
                 InitImport ii;
                 ii.rx = im.qx;
@@ -461,6 +513,13 @@ SweptPlan compile_swept_plan(int b, const Equation& eq, long m, long final_level
             return std::tie(a.seg, a.src) < std::tie(c.seg, c.src);
         });
         spread_banks(T.imports, 0, T.imports.size(), [](const Import& e) { return e.dst; });
+        if (P.colB) {
+            std::vector<int> seen(static_cast<std::size_t>(K.smem_doubles), 0);
+            for (const Import& x : T.imports) seen.at(static_cast<std::size_t>(x.dst))++;
+            for (const InitImport& x : T.inits) seen.at(static_cast<std::size_t>(x.dst))++;
+            for (int v : seen)
+                if (v > 1) fail(SG_ELOGIC, "plan: two imports share a column slot");
+        }
         return T;
     };
     int maxdelta = 0, ghost = 0;
@@ -523,7 +582,8 @@ std::string describe_plan(const SweptPlan& p) {
     os << "swept plan b=" << p.b << " n=" << p.n << " k=" << p.k << " S=" << p.S << " m=" << p.m
        << " flat=" << p.flat << " final=" << p.final_level << " launches=" << p.launches.size()
        << " classes=" << p.classes.size() << " slots=" << p.nslots << " ghost=" << p.ghost
-       << " replay_cycles=" << p.replay_cycles << "\n";
+       << " replay_cycles=" << p.replay_cycles << " heat_kernel=" << (p.colB ? "column" : "generic")
+       << " overexport=" << p.overexport << "\n";
     for (int kd = 0; kd < K_NKINDS; ++kd) {
         const KindLayout& K = p.kinds[kd];
         os << "  " << kind_name(kd) << ": levels " << K.rmin << ".." << K.nlev << " smem "

@@ -103,6 +103,10 @@ struct SweptPlan {
     int ghost = 0;         // ghost ring width in instances (max |di|,|dj|)
     int max_epad = 0;
     long replay_cycles = 0;
+    // column-register heat kernels (colgeom.hpp): block size, 0 = generic
+    // table-driven kernels; overexport = exported cells nobody reads
+    int colB = 0;
+    long overexport = 0;
     // statistics (per instance, cells): imports / exports / updates per kind
     long imports_per_kind[K_NKINDS] = {0, 0, 0, 0, 0};
     long updates_per_kind[K_NKINDS] = {0, 0, 0, 0, 0};
@@ -118,7 +122,9 @@ void lane_split(int w, int h, int* splits, int* rps);
 template <class T, class Key>
 void spread_banks(std::vector<T>& v, std::size_t begin, std::size_t end, Key key);
 
-// m = octahedra; final_level = the level the run must output.
+// m = octahedra; final_level = the level the run must output.  Heat runs with
+// b in {8, 16, 32} use the column-register kernels (colgeom.hpp) unless
+// SG_HEAT_KERNEL=generic is set in the environment.
 SweptPlan compile_swept_plan(int b, const Equation& eq, long m, long final_level);
 
 std::string describe_plan(const SweptPlan& p);
