@@ -136,6 +136,40 @@ SG_HD constexpr int exp_slot(int kind, int B, int r, int x, int y) {
     return s.has(x) ? exp_base(kind, B, r, y) + s.rank(x) : -1;
 }
 
+// Row types of a level: the distinct RowSets among its rows, in row order
+// (at most 4 for imports, 2 for exports), so the kernels evaluate each lane
+// predicate / rank once per level and address rows with immediates.
+SG_HD constexpr bool same(RowSet p, RowSet q) { return p.a == q.a && p.b == q.b && p.hp == q.hp && p.hq == q.hq; }
+template <bool IMP>
+SG_HD constexpr RowSet row_of(int kind, int B, int r, int y) {
+    return IMP ? imp_row(kind, B, r, y) : exp_row(kind, B, r, y);
+}
+// type index of row y (-1: the row is empty)
+template <bool IMP>
+SG_HD constexpr int type_of(int kind, int B, int r, int y) {
+    const RowSet s = row_of<IMP>(kind, B, r, y);
+    if (s.count() == 0) return -1;
+    int t = 0;
+    for (int yy = ylo(kind, B); yy < y; ++yy) {
+        const RowSet q = row_of<IMP>(kind, B, r, yy);
+        if (q.count() == 0) continue;
+        bool seen = false;
+        for (int zz = ylo(kind, B); zz < yy; ++zz)
+            if (row_of<IMP>(kind, B, r, zz).count() > 0 && same(row_of<IMP>(kind, B, r, zz), q)) seen = true;
+        if (seen) continue;
+        if (same(q, s)) return t;
+        ++t;
+    }
+    return t;
+}
+// the t-th distinct row set of level r (count() == 0 if none)
+template <bool IMP>
+SG_HD constexpr RowSet type_set(int kind, int B, int r, int t) {
+    for (int y = ylo(kind, B); y < ylo(kind, B) + B; ++y)
+        if (type_of<IMP>(kind, B, r, y) == t) return row_of<IMP>(kind, B, r, y);
+    return RowSet{0, 0, 0, 0};
+}
+
 SG_HD constexpr bool supported(int B) { return B == 8 || B == 16 || B == 32; }
 
 }  // namespace col

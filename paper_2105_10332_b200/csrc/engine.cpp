@@ -165,6 +165,7 @@ void Solver::build_swept() {
     const int pbx = pw_ / b, pby = ph_ / b;
     const int g = P.ghost, extw = pbx + 2 * g, exth = pby + 2 * g;
     const std::size_t rec_len = static_cast<std::size_t>(extw) * exth * nv * P.max_epad;
+    rec_len_ = rec_len;
     const std::size_t plane = static_cast<std::size_t>(pw_) * ph_;
 
     // one instance's phase must fit on chip (levels + Euler flux scratch)
@@ -199,8 +200,11 @@ void Solver::build_swept() {
         if (frame_ring_ > 0) pb.frames = dev_alloc<double>(d, static_cast<std::size_t>(frame_ring_) * plane * nv);
         pb.init = dev_alloc<double>(d, plane * nv);
         pb.out = dev_alloc<double>(d, plane * nv);
+        // one allocation per partition, slot s at s * rec_len (the column
+        // kernels address every producer record from the instance's slot-0 base)
         pb.rec.resize(P.nslots);
-        for (int s = 0; s < P.nslots; ++s) pb.rec[s] = dev_alloc<double>(d, std::max<std::size_t>(rec_len, 1));
+        double* all = dev_alloc<double>(d, std::max<std::size_t>(rec_len * P.nslots, 1));
+        for (int s = 0; s < P.nslots; ++s) pb.rec[s] = all + rec_len * s;
         // level-0 piece of this partition (engine.cpp:199-209 load_initial)
         std::vector<double> piece(plane * nv);
         for (int v = 0; v < nv; ++v)
@@ -267,6 +271,12 @@ void Solver::finalize_swept() {
                 im2.push_back(make_int2((x.seg << 20) | x.src, x.dst));
             }
             d.d_imp2.push_back(dev_upload(d, im2));
+            std::vector<unsigned> pk;
+            for (const Import& x : T.imports) {
+                if (x.src >= (1 << 16) || x.dst >= (1 << 16)) fail(SG_ELOGIC, "swept: packed import table overflow");
+                pk.push_back((static_cast<unsigned>(x.src) << 16) | static_cast<unsigned>(x.dst));
+            }
+            d.d_imp_packed.push_back(dev_upload(d, pk));
             for (const InitImport& x : T.inits) in.push_back(make_int4(x.rx, x.ry, x.dst, x.vstride));
             d.d_imp.push_back(dev_upload(d, im));
             d.d_init.push_back(dev_upload(d, in));
@@ -309,7 +319,7 @@ void Solver::finalize_swept() {
                 a.fx_doubles = (fx + 1) & ~1;
             }
             a.nexp_early = K.nexp_early;
-            a.epad = K.epad;
+            a.epad = P.max_epad;  // uniform record stride per instance (all kinds)
             a.lev = d.d_lev[L.kind];
             a.exp_off = d.d_exp_off[L.kind];
             a.exp_vs = d.d_exp_vs[L.kind];
@@ -318,6 +328,27 @@ void Solver::finalize_swept() {
             a.pitch = d.d_pitch[L.kind];
             a.imports = d.d_imp[L.cls];
             a.imports2 = d.d_imp2[L.cls];
+            a.imp_packed = d.d_imp_packed[L.cls];
+            if (P.colB) {
+                // imports as signed offsets from the consumer instance's slot-0
+                // record base: producer slot * rec_len + (dj*extw + di)*stride + src
+                const int rot = static_cast<int>(li % P.nslots);
+                auto key = std::make_pair(L.cls, rot);
+                auto it = d.imp_off.find(key);
+                if (it == d.imp_off.end()) {
+                    std::vector<int2> tab;
+                    for (const Import& x : T.imports) {
+                        const Segment& sg = T.segs[x.seg];
+                        const long pslot = ((static_cast<long>(li) - sg.delta) % P.nslots + P.nslots) % P.nslots;
+                        const long off = pslot * static_cast<long>(rec_len_) +
+                                         (static_cast<long>(sg.dj) * extw + sg.di) * P.max_epad + x.src;
+                        if (off > INT32_MAX || off < INT32_MIN) fail(SG_ELOGIC, "swept: record offset overflow");
+                        tab.push_back(make_int2(static_cast<int>(off), x.dst));
+                    }
+                    it = d.imp_off.emplace(key, dev_upload(d, tab)).first;
+                }
+                a.imp_off = it->second;
+            }
             a.nimp = static_cast<int>(T.imports.size());
             a.inits = d.d_init[L.cls];
             a.ninit = static_cast<int>(T.inits.size());
@@ -325,7 +356,16 @@ void Solver::finalize_swept() {
             for (std::size_t s = 0; s < T.segs.size(); ++s) {
                 const long pl = static_cast<long>(li) - T.segs[s].delta;
                 if (pl < 0 || P.launches[pl].slot < 0) fail(SG_ELOGIC, "swept: import from a launch without record");
-                a.segs[s] = {P.launches[pl].slot, T.segs[s].di, T.segs[s].dj, P.kinds[T.segs[s].pkind].epad};
+                int beg = static_cast<int>(T.imports.size()), end = 0;
+                for (std::size_t q = 0; q < T.imports.size(); ++q)
+                    if (T.imports[q].seg == static_cast<int>(s)) {
+                        beg = std::min(beg, static_cast<int>(q));
+                        end = std::max(end, static_cast<int>(q) + 1);
+                    }
+                if (beg > end) beg = end = 0;
+                for (int q = beg; P.colB && q < end; ++q)
+                    if (T.imports[q].seg != static_cast<int>(s)) fail(SG_ELOGIC, "swept: import segment not contiguous");
+                a.segs[s] = {P.launches[pl].slot, T.segs[s].di, T.segs[s].dj, P.max_epad, beg, end};
             }
             a.nsegs = static_cast<int>(T.segs.size());
             a.frame = L.frame;
@@ -732,7 +772,7 @@ std::vector<unsigned char> Solver::ipc_blob() const {
     const PartBuffers& pb = parts_[rank_];
     std::vector<void*> bufs;
     if (cfg_.engine == SG_SWEPT) {
-        for (double* r : pb.rec) bufs.push_back(r);
+        bufs.push_back(pb.rec[0]);  // all slots: one allocation
         bufs.push_back(pb.init);
         bufs.push_back(pb.out);
     } else {
@@ -769,7 +809,8 @@ void Solver::connect(const unsigned char* blobs, std::size_t per_rank) {
         int i = 0;
         if (cfg_.engine == SG_SWEPT) {
             pb.rec.resize(plan_.nslots);
-            for (int s2 = 0; s2 < plan_.nslots; ++s2) pb.rec[s2] = static_cast<double*>(p[i++]);
+            double* all = static_cast<double*>(p[i++]);
+            for (int s2 = 0; s2 < plan_.nslots; ++s2) pb.rec[s2] = all + rec_len_ * s2;
             pb.init = static_cast<double*>(p[i++]);
             pb.out = static_cast<double*>(p[i++]);
         } else {

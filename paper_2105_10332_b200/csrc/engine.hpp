@@ -5,7 +5,9 @@
 
 #include <cuda_runtime.h>
 
+#include <map>
 #include <memory>
+#include <utility>
 #include <vector>
 
 #include "kernels.cuh"
@@ -44,6 +46,8 @@ struct DeviceCtx {
     int2* d_pitch[K_NKINDS] = {};
     std::vector<int4*> d_imp, d_init;
     std::vector<int2*> d_imp2;
+    std::vector<unsigned*> d_imp_packed;
+    std::map<std::pair<int, int>, int2*> imp_off;  // (class, slot rotation) -> column gather table
     double** d_rec_tab = nullptr;
     double** d_frames_tab = nullptr;
     const double** d_init_tab = nullptr;
@@ -111,6 +115,7 @@ class Solver {
     std::string snap_path_;
     long snap_every_ = 1;
     int frame_ring_ = 0;
+    std::size_t rec_len_ = 0;     // doubles per record slot (all slots contiguous)
     std::vector<std::vector<long>> done_after_;  // swept: levels completed by launch i
     long snapshot_frames_ = 0;
     void snapshot_frame(SnapshotWriter& w, long level, int slot_or_ring);  // D2H + assemble + append

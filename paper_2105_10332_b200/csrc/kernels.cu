@@ -52,6 +52,11 @@ __device__ __forceinline__ int2 ldg_keep(const int2* p) {
     asm("ld.global.nc.L1::evict_last.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
     return v;
 }
+__device__ __forceinline__ unsigned ldg_keep(const unsigned* p) {
+    unsigned v;
+    asm("ld.global.nc.L1::evict_last.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
 __device__ __forceinline__ int ldg_keep(const int* p) {
     int v;
     asm("ld.global.nc.L1::evict_last.s32 %0, [%1];" : "=r"(v) : "l"(p));
@@ -233,6 +238,17 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_kernel(const __grid_const
     if (A.nexp > A.nexp_early) flush(A.nexp_early, A.nexp);
 }
 
+// Predicated shared load / global store (one instruction, no branch).
+__device__ __forceinline__ void lds_if(double& v, unsigned saddr, bool p) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.shared.f64 %0, [%1];\n\t}"
+                 : "+d"(v)
+                 : "r"(saddr), "r"(static_cast<int>(p)));
+}
+__device__ __forceinline__ void stg_if(double* g, double v, bool p) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.f64 [%0], %1;\n\t}" ::"l"(g), "d"(v),
+                 "r"(static_cast<int>(p)));
+}
+
 // Compile-time loop: f(std::integral_constant<int, I>) for I = 0..N-1.
 template <class F, int... I>
 __device__ __forceinline__ void sfor_impl(F&& f, std::integer_sequence<int, I...>) {
@@ -263,63 +279,59 @@ __device__ __noinline__ void put_column(const SweptArgs& A, const double* stash,
 }
 
 // Heat phase kernel, column-register form (block B in {8, 16, 32}, geometry
-// in colgeom.hpp).  B lanes own one phase instance (32/B instances per warp,
-// 4 warps per CTA); lane c holds column c of the instance's B x B window in
-// registers, v[i] = row ylo + i of the current level.  Per level r (all
-// geometry is compile-time, levels and rows fully unrolled):
+// in colgeom.hpp).  L = B/CPL lanes own one phase instance (32/L instances
+// per warp, WPC warps per CTA); lane l holds columns CPL*l .. CPL*l+CPL-1 of
+// the instance's B x B window in registers, v[q][i] = row ylo + i of column
+// CPL*l+q at the current level.  Per level r (all geometry compile-time,
+// levels and rows fully unrolled):
 //   1. imports: the cells of level r-1 this instance did not compute come
 //      from shared memory, where the gather landed them (one predicated LDS
-//      per row; lanes whose cells are imports take them);
-//   2. update rows [y0, y1) of R_r in place: north/south/centre are the
-//      lane's own registers, east/west come from lanes c+1 / c-1 by warp
-//      shuffle (heat_point, physics.hpp:57-63; no FMA);
+//      per row and column; lanes whose cells are imports take them);
+//   2. update rows [y0, y1) of R_r in place: north/south/centre and the
+//      lane's inner east/west neighbours are registers; the outer ones come
+//      from lanes l-1 / l+1 by warp shuffle (heat_point, physics.hpp:57-63;
+//      no FMA);
 //   3. exports: the cells of R_r that other instances read go straight from
-//      registers into this instance's record (contiguous per row).
+//      registers into this instance's record (one predicated store per row).
 // Lanes outside R_r compute too (SIMT); their rows are never read before an
 // import overwrites them.  Nothing but the imports touches shared memory.
-template <int B, int KIND>
-__global__ void __launch_bounds__(128) swept_heat_col_kernel(const __grid_constant__ SweptArgs A) {
-    constexpr int IPW = 32 / B;
+template <int B, int KIND, int CPL, int WPC, int MINB>
+__global__ void __launch_bounds__(WPC * 32, MINB) swept_heat_col_kernel(const __grid_constant__ SweptArgs A) {
+    constexpr int L = B / CPL;       // lanes per instance
+    constexpr int IPW = 32 / L;      // instances per warp
     constexpr int NL = col::nlev(KIND, B);
     constexpr int YLO = col::ylo(KIND, B);
     extern __shared__ double sm[];
-    __shared__ const double* segbase[4 * IPW][kMaxSegs];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int sub = lane / B, c = lane % B;
+    const int sub = lane / L, l = lane % L;
     const int slot_in_cta = warp * IPW + sub;
     const int ninst = A.pbx * A.pby;
-    const int inst = blockIdx.x * (4 * IPW) + slot_in_cta;
+    const int inst = blockIdx.x * (WPC * IPW) + slot_in_cta;
     const bool live = inst < ninst;
     const int part = A.dev_parts[blockIdx.y];
     const int pi = part % A.px, pj = part / A.px;
     const int bi = live ? inst % A.pbx : 0, bj = live ? inst / A.pbx : 0;
     const int half = A.frame * (B / 2);
+    const int gh = A.ghost;
     double* S = sm + slot_in_cta * A.smem_doubles;
-    const double** sb = segbase[slot_in_cta];
 
-    // ---- gather the imports (records of earlier phases, initial plane)
-    if (live)
-        for (int s = c; s < A.nsegs; s += B) {
-            const DevSeg sg = A.segs[s];
-            const long ext = (long)(bj + sg.dj + A.ghost) * A.extw + (bi + sg.di + A.ghost);
-            sb[s] = A.rec[part * A.nslots + sg.slot] + ext * sg.epad;
-        }
-    __syncwarp();
+    // ---- gather the imports: {offset from this instance's slot-0 record, smem slot}
     if (live) {
-        int i = c;
-        for (; i + 3 * B < A.nimp; i += 4 * B) {
-            const int2 e0 = ldg_keep(&A.imports2[i]), e1 = ldg_keep(&A.imports2[i + B]);
-            const int2 e2 = ldg_keep(&A.imports2[i + 2 * B]), e3 = ldg_keep(&A.imports2[i + 3 * B]);
-            cp_async8(S + e0.y, sb[e0.x >> 20] + (e0.x & 0xFFFFF));
-            cp_async8(S + e1.y, sb[e1.x >> 20] + (e1.x & 0xFFFFF));
-            cp_async8(S + e2.y, sb[e2.x >> 20] + (e2.x & 0xFFFFF));
-            cp_async8(S + e3.y, sb[e3.x >> 20] + (e3.x & 0xFFFFF));
+        const double* ibase = A.rec[part * A.nslots] + ((long)(bj + gh) * A.extw + (bi + gh)) * A.epad;
+        int i = l;
+        for (; i + 3 * L < A.nimp; i += 4 * L) {
+            const int2 e0 = ldg_keep(&A.imp_off[i]), e1 = ldg_keep(&A.imp_off[i + L]);
+            const int2 e2 = ldg_keep(&A.imp_off[i + 2 * L]), e3 = ldg_keep(&A.imp_off[i + 3 * L]);
+            cp_async8(S + e0.y, ibase + e0.x);
+            cp_async8(S + e1.y, ibase + e1.x);
+            cp_async8(S + e2.y, ibase + e2.x);
+            cp_async8(S + e3.y, ibase + e3.x);
         }
-        for (; i < A.nimp; i += B) {
-            const int2 e = ldg_keep(&A.imports2[i]);
-            cp_async8(S + e.y, sb[e.x >> 20] + (e.x & 0xFFFFF));
+        for (; i < A.nimp; i += L) {
+            const int2 e = ldg_keep(&A.imp_off[i]);
+            cp_async8(S + e.y, ibase + e.x);
         }
-        for (int j = c; j < A.ninit; j += B) {
+        for (int j = l; j < A.ninit; j += L) {
             const int4 im = __ldg(&A.inits[j]);
             const int gx = wrapi(pi * A.pw + bi * B - half + im.x, A.nx);
             const int gy = wrapi(pj * A.ph + bj * B - half + im.y, A.ny);
@@ -330,69 +342,119 @@ __global__ void __launch_bounds__(128) swept_heat_col_kernel(const __grid_consta
     cp_async_wait_all();
     __syncwarp();
 
-    const int gh = A.ghost;
     double* dst = A.rec[part * A.nslots + A.my_slot] + ((long)(bj + gh) * A.extw + (bi + gh)) * A.epad;
     const double fx = A.c0, fy = A.c1;
+    const unsigned s_imp = static_cast<unsigned>(__cvta_generic_to_shared(S));
     // output stash (only allocated by launches that write the output level or snapshots)
-    double* stash = sm + 4 * IPW * A.smem_doubles + (slot_in_cta * B + c) * B;
-    double v[B];
+    double* stash = sm + WPC * IPW * A.smem_doubles + (slot_in_cta * L + l) * CPL * B;
+    double v[CPL][B];
 #pragma unroll
-    for (int i = 0; i < B; ++i) v[i] = 0.0;
+    for (int q = 0; q < CPL; ++q)
+#pragma unroll
+        for (int i = 0; i < B; ++i) v[q][i] = 0.0;
 
     sfor<NL>([&](auto RI) {
         constexpr int r = decltype(RI)::value + 1;
-        constexpr col::CRect q = col::rect(KIND, B, r);
-        // 1. imports of level r-1
-        sfor<B>([&](auto YI) {
-            constexpr int j = decltype(YI)::value;
-            constexpr col::RowSet is = col::imp_row(KIND, B, r, YLO + j);
-            if constexpr (is.count() > 0) {
-                constexpr int base = col::imp_base(KIND, B, r, YLO + j);
-                if (is.has(c)) v[j] = S[base + is.rank(c)];
-            }
-        });
-        // 2. rows [y0, y1) of R_r, in place (prev = the old value of the row below)
-        double prev = v[q.y0 - 1 - YLO];
-        sfor<B>([&](auto YI) {
-            constexpr int j = decltype(YI)::value;
-            constexpr col::CRect qr = col::rect(KIND, B, r);
-            if constexpr (YLO + j >= qr.y0 && YLO + j < qr.y1) {
-                const double cur = v[j];
-                const double e = __shfl_down_sync(0xffffffffu, cur, 1);
-                const double w = __shfl_up_sync(0xffffffffu, cur, 1);
-                const double nv = heat_update(cur, e, w, v[j + 1], prev, fx, fy);
-                prev = cur;
-                v[j] = nv;
-            }
-        });
-        // 3. exports of level r
-        if (live)
-            sfor<B>([&](auto YI) {
-                constexpr int j = decltype(YI)::value;
-                constexpr col::RowSet es = col::exp_row(KIND, B, r, YLO + j);
-                if constexpr (es.count() > 0) {
-                    constexpr int base = col::exp_base(KIND, B, r, YLO + j);
-                    if (es.has(c)) dst[base + es.rank(c)] = v[j];
+        // 1. imports of level r-1: lane predicate / address once per row type
+        {
+            bool ip[CPL][4];
+            unsigned ia[CPL][4];
+            sfor<4>([&](auto TI) {
+                constexpr int t = decltype(TI)::value;
+                constexpr col::RowSet ts = col::type_set<true>(KIND, B, r, t);
+#pragma unroll
+                for (int q = 0; q < CPL; ++q) {
+                    const int c = CPL * l + q;
+                    ip[q][t] = ts.count() > 0 && ts.has(c);
+                    ia[q][t] = s_imp + 8u * static_cast<unsigned>(ts.count() > 0 ? ts.rank(c) : 0);
                 }
             });
-        // output level / snapshot (rare): the lane's column goes through its
+            sfor<B>([&](auto YI) {
+                constexpr int j = decltype(YI)::value;
+                constexpr int t = col::type_of<true>(KIND, B, r, YLO + j);
+                if constexpr (t >= 0) {
+                    constexpr int base = col::imp_base(KIND, B, r, YLO + j);
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) lds_if(v[q][j], ia[q][t] + 8u * base, ip[q][t]);
+                }
+            });
+        }
+        // 2. rows [y0, y1) of R_r, in place (prev = the old values of the row below)
+        {
+            constexpr col::CRect q0 = col::rect(KIND, B, r);
+            double prev[CPL];
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) prev[q] = v[q][q0.y0 - 1 - YLO];
+            sfor<B>([&](auto YI) {
+                constexpr int j = decltype(YI)::value;
+                constexpr col::CRect qr = col::rect(KIND, B, r);
+                if constexpr (YLO + j >= qr.y0 && YLO + j < qr.y1) {
+                    double cur[CPL];
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) cur[q] = v[q][j];
+                    const double east = __shfl_down_sync(0xffffffffu, cur[0], 1);
+                    const double west = __shfl_up_sync(0xffffffffu, cur[CPL - 1], 1);
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) {
+                        const double e = q + 1 < CPL ? cur[q + 1 < CPL ? q + 1 : 0] : east;
+                        const double w = q > 0 ? cur[q > 0 ? q - 1 : 0] : west;
+                        v[q][j] = heat_update(cur[q], e, w, v[q][j + 1], prev[q], fx, fy);
+                        prev[q] = cur[q];
+                    }
+                }
+            });
+        }
+        // 3. exports of level r (row types: full rows, rows with the hole)
+        if (live) {
+            bool ep[CPL][2];
+            double* eg[CPL][2];
+            sfor<2>([&](auto TI) {
+                constexpr int t = decltype(TI)::value;
+                constexpr col::RowSet ts = col::type_set<false>(KIND, B, r, t);
+#pragma unroll
+                for (int q = 0; q < CPL; ++q) {
+                    const int c = CPL * l + q;
+                    ep[q][t] = ts.count() > 0 && ts.has(c);
+                    eg[q][t] = dst + (ts.count() > 0 ? ts.rank(c) : 0);
+                }
+            });
+            sfor<B>([&](auto YI) {
+                constexpr int j = decltype(YI)::value;
+                constexpr int t = col::type_of<false>(KIND, B, r, YLO + j);
+                static_assert(t < 2, "export row types");
+                if constexpr (t >= 0) {
+                    constexpr int base = col::exp_base(KIND, B, r, YLO + j);
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) stg_if(eg[q][t] + base, v[q][j], ep[q][t]);
+                }
+            });
+        }
+        // output level / snapshot (rare): the lane's columns go through its
         // shared-memory stash to a non-inlined writer (keeps the unrolled
         // level code small)
         if (((A.out_mask | A.snap_mask) >> r) & 1ull) {
+            constexpr col::CRect qr = col::rect(KIND, B, r);
 #pragma unroll
-            for (int i = 0; i < B; ++i) stash[i] = v[i];
-            if (live && c >= q.x0 && c < q.x1)
-                put_column(A, stash, c, q.y0 - YLO, q.y1 - YLO, YLO, pi, pj, bi * B - half + c, bj * B - half,
-                           A.lo + r - 1, (A.out_mask >> r) & 1ull, (A.snap_mask >> r) & 1ull);
+            for (int q = 0; q < CPL; ++q)
+#pragma unroll
+                for (int i = 0; i < B; ++i) stash[q * B + i] = v[q][i];
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) {
+                const int c = CPL * l + q;
+                if (live && c >= qr.x0 && c < qr.x1)
+                    put_column(A, stash + q * B, c, qr.y0 - YLO, qr.y1 - YLO, YLO, pi, pj, bi * B - half + c,
+                               bj * B - half, A.lo + r - 1, (A.out_mask >> r) & 1ull, (A.snap_mask >> r) & 1ull);
+            }
         }
     });
 
     // ---- partition-edge instances: copy the record into the neighbours' ghost rings
     const bool edge = bi < gh || bi >= A.pbx - gh || bj < gh || bj >= A.pby - gh;
     if (edge && live && A.nexp > 0) {
-        if constexpr (B == 32) __syncwarp();
-        else __syncwarp(((1u << B) - 1u) << (sub * B));
-        for (int e = c; e < A.nexp; e += B) {
+        asm volatile("" ::: "memory");
+        if constexpr (L == 32) __syncwarp();
+        else __syncwarp(((1u << L) - 1u) << (sub * L));
+        for (int e = l; e < A.nexp; e += L) {
             const double val = __ldcg(dst + e);
             for (int ej = -1; ej <= 1; ++ej)
                 for (int ei = -1; ei <= 1; ++ei) {
@@ -769,24 +831,29 @@ cudaError_t launch_dist_barrier(unsigned long long* const* peer_flags, unsigned 
     return cudaGetLastError();
 }
 
+#ifndef SG_COL_CPL
+#define SG_COL_CPL 1
+#endif
 template <int B>
 cudaError_t launch_heat_col(const SweptArgs& a, cudaStream_t s) {
-    constexpr int IPC = 4 * (32 / B);  // instances per CTA
+    constexpr int CPL = SG_COL_CPL;             // columns per lane
+    constexpr int WPC = 4;                      // warps per CTA
+    constexpr int IPC = WPC * (32 / (B / CPL));  // instances per CTA
     const bool stash = (a.out_mask | a.snap_mask) != 0ull;
     const size_t smem = static_cast<size_t>(IPC) * (a.smem_doubles + (stash ? B * B : 0)) * sizeof(double);
     const int ninst = a.pbx * a.pby;
     dim3 grid((ninst + IPC - 1) / IPC, a.ndev_parts);
     auto go = [&](auto kern) {
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<grid, 128, smem, s>>>(a);
+        kern<<<grid, WPC * 32, smem, s>>>(a);
         return cudaGetLastError();
     };
     switch (a.kind) {
-        case col::UP: return go(swept_heat_col_kernel<B, col::UP>);
-        case col::YB: return go(swept_heat_col_kernel<B, col::YB>);
-        case col::XB: return go(swept_heat_col_kernel<B, col::XB>);
-        case col::OCT: return go(swept_heat_col_kernel<B, col::OCT>);
-        default: return go(swept_heat_col_kernel<B, col::DOWN>);
+        case col::UP: return go(swept_heat_col_kernel<B, col::UP, CPL, WPC, 1>);
+        case col::YB: return go(swept_heat_col_kernel<B, col::YB, CPL, WPC, 1>);
+        case col::XB: return go(swept_heat_col_kernel<B, col::XB, CPL, WPC, 1>);
+        case col::OCT: return go(swept_heat_col_kernel<B, col::OCT, CPL, WPC, 1>);
+        default: return go(swept_heat_col_kernel<B, col::DOWN, CPL, WPC, 1>);
     }
 }
 

@@ -512,7 +512,8 @@ SweptPlan compile_swept_plan(int b, const Equation& eq, long m, long final_level
         std::sort(T.imports.begin(), T.imports.end(), [](const Import& a, const Import& c) {
             return std::tie(a.seg, a.src) < std::tie(c.seg, c.src);
         });
-        spread_banks(T.imports, 0, T.imports.size(), [](const Import& e) { return e.dst; });
+        // column kernels gather segment by segment: keep the (seg, src) order
+        if (!P.colB) spread_banks(T.imports, 0, T.imports.size(), [](const Import& e) { return e.dst; });
         if (P.colB) {
             std::vector<int> seen(static_cast<std::size_t>(K.smem_doubles), 0);
             for (const Import& x : T.imports) seen.at(static_cast<std::size_t>(x.dst))++;
