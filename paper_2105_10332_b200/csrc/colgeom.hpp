@@ -170,6 +170,63 @@ SG_HD constexpr RowSet type_set(int kind, int B, int r, int t) {
     return RowSet{0, 0, 0, 0};
 }
 
+// All of the above for one (kind, B), evaluated once per kernel instantiation
+// (the kernels index these tables in constant expressions; recomputing the
+// loops above at every use made the device build slow).
+constexpr int kMaxB = 32;
+constexpr int kMaxNL = 2 * (kMaxB / 2 - 1);
+struct Tables {
+    RowSet imp[kMaxNL + 1][kMaxB], exp[kMaxNL + 1][kMaxB];
+    int imp_base[kMaxNL + 2][kMaxB], exp_base[kMaxNL + 2][kMaxB];
+    int imp_type[kMaxNL + 1][kMaxB], exp_type[kMaxNL + 1][kMaxB];
+    RowSet imp_tset[kMaxNL + 1][4], exp_tset[kMaxNL + 1][2];
+};
+template <int NT>
+SG_HD constexpr void fill_types(const RowSet (&rows)[kMaxNL + 1][kMaxB], int nl, int B, int (&type)[kMaxNL + 1][kMaxB],
+                                RowSet (&tset)[kMaxNL + 1][NT]) {
+    for (int r = 1; r <= nl; ++r) {
+        RowSet seen[kMaxB] = {};
+        int n = 0;
+        for (int i = 0; i < B; ++i) {
+            const RowSet s = rows[r][i];
+            type[r][i] = -1;
+            if (s.count() == 0) continue;
+            int t = -1;
+            for (int u = 0; u < n; ++u)
+                if (same(seen[u], s)) t = u;
+            if (t < 0) {
+                t = n;
+                seen[n++] = s;
+            }
+            type[r][i] = t;
+        }
+        for (int u = 0; u < NT; ++u) tset[r][u] = u < n ? seen[u] : RowSet{0, 0, 0, 0};
+    }
+}
+SG_HD constexpr Tables make_tables(int kind, int B) {
+    Tables t{};
+    const int nl = nlev(kind, B), y0 = ylo(kind, B);
+    int si = 0, se = 0;
+    for (int r = 1; r <= nl + 1; ++r)
+        for (int i = 0; i < B; ++i) {
+            t.imp_base[r][i] = si;
+            t.exp_base[r][i] = se;
+            if (r <= nl) {
+                t.imp[r][i] = imp_row(kind, B, r, y0 + i);
+                t.exp[r][i] = exp_row(kind, B, r, y0 + i);
+                si += t.imp[r][i].count();
+                se += t.exp[r][i].count();
+            }
+        }
+    fill_types<4>(t.imp, nl, B, t.imp_type, t.imp_tset);
+    fill_types<2>(t.exp, nl, B, t.exp_type, t.exp_tset);
+    return t;
+}
+template <int KIND, int B>
+struct Geo {
+    static constexpr Tables t = make_tables(KIND, B);
+};
+
 SG_HD constexpr bool supported(int B) { return B == 8 || B == 16 || B == 32; }
 
 }  // namespace col

@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(WPC * 32, MINB) swept_heat_col_kernel(const __
             unsigned ia[CPL][4];
             sfor<4>([&](auto TI) {
                 constexpr int t = decltype(TI)::value;
-                constexpr col::RowSet ts = col::type_set<true>(KIND, B, r, t);
+                constexpr col::RowSet ts = col::Geo<KIND, B>::t.imp_tset[r][t];
 #pragma unroll
                 for (int q = 0; q < CPL; ++q) {
                     const int c = CPL * l + q;
@@ -371,9 +371,9 @@ __global__ void __launch_bounds__(WPC * 32, MINB) swept_heat_col_kernel(const __
             });
             sfor<B>([&](auto YI) {
                 constexpr int j = decltype(YI)::value;
-                constexpr int t = col::type_of<true>(KIND, B, r, YLO + j);
+                constexpr int t = col::Geo<KIND, B>::t.imp_type[r][j];
                 if constexpr (t >= 0) {
-                    constexpr int base = col::imp_base(KIND, B, r, YLO + j);
+                    constexpr int base = col::Geo<KIND, B>::t.imp_base[r][j];
 #pragma unroll
                     for (int q = 0; q < CPL; ++q) lds_if(v[q][j], ia[q][t] + 8u * base, ip[q][t]);
                 }
@@ -410,7 +410,7 @@ __global__ void __launch_bounds__(WPC * 32, MINB) swept_heat_col_kernel(const __
             double* eg[CPL][2];
             sfor<2>([&](auto TI) {
                 constexpr int t = decltype(TI)::value;
-                constexpr col::RowSet ts = col::type_set<false>(KIND, B, r, t);
+                constexpr col::RowSet ts = col::Geo<KIND, B>::t.exp_tset[r][t];
 #pragma unroll
                 for (int q = 0; q < CPL; ++q) {
                     const int c = CPL * l + q;
@@ -420,10 +420,10 @@ __global__ void __launch_bounds__(WPC * 32, MINB) swept_heat_col_kernel(const __
             });
             sfor<B>([&](auto YI) {
                 constexpr int j = decltype(YI)::value;
-                constexpr int t = col::type_of<false>(KIND, B, r, YLO + j);
+                constexpr int t = col::Geo<KIND, B>::t.exp_type[r][j];
                 static_assert(t < 2, "export row types");
                 if constexpr (t >= 0) {
-                    constexpr int base = col::exp_base(KIND, B, r, YLO + j);
+                    constexpr int base = col::Geo<KIND, B>::t.exp_base[r][j];
 #pragma unroll
                     for (int q = 0; q < CPL; ++q) stg_if(eg[q][t] + base, v[q][j], ep[q][t]);
                 }
