@@ -139,7 +139,9 @@ int sg_solver_upload(sg_solver* s, const double* host, char* err, size_t errlen)
 int sg_solver_download(sg_solver* s, double* host, char* err, size_t errlen);
 /* The initial condition make_setup computed (engine.cpp:27-70), [var][ny][nx]. */
 int sg_solver_initial(sg_solver* s, double* host, char* err, size_t errlen);
-/* Enable (1) / disable (0) per-launch CUDA events around the dominant kernel. */
+/* Enable (1) / disable (0) per-launch CUDA events around the dominant kernel;
+ * 2 + k times the launches of swept phase kind k instead (0 UpPyramid,
+ * 1 YBridge, 2 XBridge, 3 Octahedron, 4 DownPyramid). */
 int sg_solver_set_profile(sg_solver* s, int on);
 void sg_solver_destroy(sg_solver* s);
 

@@ -312,7 +312,7 @@ class Solver:
     """Resident solver (sg_solver_*): create once, then reset/solve/fetch.
     Used by bench.py to time the solve with inputs already in HBM."""
 
-    def __init__(self, cfg: SolverConfig, profile: bool = False, _dist=None):
+    def __init__(self, cfg: SolverConfig, profile=False, _dist=None):
         self._L = _c.load()
         self._cfg = cfg._c()
         h = C.c_void_p()
@@ -323,8 +323,8 @@ class Solver:
             rank, world = _dist
             _check(self._L.sg_dist_create(C.byref(self._cfg), rank, world, C.byref(h), err, len(err)), err)
         self._h = h
-        if profile:
-            self._L.sg_solver_set_profile(self._h, 1)
+        if profile:  # True: the dominant kernel; an int k >= 2: swept phase kind k - 2
+            self._L.sg_solver_set_profile(self._h, int(profile))
 
     def reset(self) -> None:
         err = _c.errbuf()

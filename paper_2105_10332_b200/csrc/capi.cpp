@@ -166,6 +166,7 @@ int sg_solver_initial(sg_solver* s, double* host, char* err, size_t errlen) {
 
 int sg_solver_set_profile(sg_solver* s, int on) {
     s->s->profile = on != 0;
+    if (on >= 2) s->s->set_prof_kind(on - 2);  // 2 + phase kind: time that kind's launches
     return SG_OK;
 }
 

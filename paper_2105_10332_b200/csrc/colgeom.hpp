@@ -170,13 +170,42 @@ SG_HD constexpr RowSet type_set(int kind, int B, int r, int t) {
     return RowSet{0, 0, 0, 0};
 }
 
+// Lane mode per level: COL (lane = column, registers = rows) or ROW (lane =
+// row, registers = columns), whichever iterates fewer registers: the bridges
+// start wide-and-short and end narrow-and-tall (YBridge) or the reverse
+// (XBridge), so each switches once; the pyramids and the octahedron stay COL.
+constexpr int COL = 0, ROW = 1;
+SG_HD constexpr int mode(int kind, int B, int r) {
+    const CRect q = rect(kind, B, r);
+    if (empty(q)) return COL;
+    return (q.x1 - q.x0) < (q.y1 - q.y0) ? ROW : COL;
+}
+// transpose tile (cells of R_r at a mode switch after level r), doubles
+SG_HD constexpr int tile_doubles(int kind, int B) {
+    int m = 0;
+    for (int r = 1; r < nlev(kind, B); ++r)
+        if (mode(kind, B, r) != mode(kind, B, r + 1)) {
+            const CRect q = rect(kind, B, r);
+            const int a = (q.x1 - q.x0) * (q.y1 - q.y0);
+            m = a > m ? a : m;
+        }
+    return m;
+}
+
 // All of the above for one (kind, B), evaluated once per kernel instantiation
 // (the kernels index these tables in constant expressions; recomputing the
 // loops above at every use made the device build slow).
 constexpr int kMaxB = 32;
 constexpr int kMaxNL = 2 * (kMaxB / 2 - 1);
+// a run of consecutive window rows i in [i0, i1) of the same row type t whose
+// first slot is base and which hold cnt cells each (ROW-mode lane lookup)
+struct Run {
+    int i0, i1, t, base, cnt;
+};
+constexpr int kMaxRuns = 6;
 struct Tables {
     RowSet imp[kMaxNL + 1][kMaxB], exp[kMaxNL + 1][kMaxB];
+    Run imp_runs[kMaxNL + 1][kMaxRuns], exp_runs[kMaxNL + 1][kMaxRuns];
     int imp_base[kMaxNL + 2][kMaxB], exp_base[kMaxNL + 2][kMaxB];
     int imp_type[kMaxNL + 1][kMaxB], exp_type[kMaxNL + 1][kMaxB];
     RowSet imp_tset[kMaxNL + 1][4], exp_tset[kMaxNL + 1][2];
@@ -203,6 +232,23 @@ SG_HD constexpr void fill_types(const RowSet (&rows)[kMaxNL + 1][kMaxB], int nl,
         for (int u = 0; u < NT; ++u) tset[r][u] = u < n ? seen[u] : RowSet{0, 0, 0, 0};
     }
 }
+SG_HD constexpr void fill_runs(const int (&type)[kMaxNL + 1][kMaxB], const int (&base)[kMaxNL + 2][kMaxB],
+                               const RowSet (&rows)[kMaxNL + 1][kMaxB], int nl, int B,
+                               Run (&runs)[kMaxNL + 1][kMaxRuns]) {
+    for (int r = 1; r <= nl; ++r) {
+        int n = 0;
+        for (int u = 0; u < kMaxRuns; ++u) runs[r][u] = Run{0, 0, -1, 0, 0};
+        for (int i = 0; i < B; ++i) {
+            if (type[r][i] < 0) continue;
+            if (n > 0 && runs[r][n - 1].i1 == i && runs[r][n - 1].t == type[r][i]) {
+                runs[r][n - 1].i1 = i + 1;
+                continue;
+            }
+            if (n == kMaxRuns) return;  // (never for the supported kinds; checked by static_assert in the kernel)
+            runs[r][n++] = Run{i, i + 1, type[r][i], base[r][i], rows[r][i].count()};
+        }
+    }
+}
 SG_HD constexpr Tables make_tables(int kind, int B) {
     Tables t{};
     const int nl = nlev(kind, B), y0 = ylo(kind, B);
@@ -220,6 +266,8 @@ SG_HD constexpr Tables make_tables(int kind, int B) {
         }
     fill_types<4>(t.imp, nl, B, t.imp_type, t.imp_tset);
     fill_types<2>(t.exp, nl, B, t.exp_type, t.exp_tset);
+    fill_runs(t.imp_type, t.imp_base, t.imp, nl, B, t.imp_runs);
+    fill_runs(t.exp_type, t.exp_base, t.exp, nl, B, t.exp_runs);
     return t;
 }
 template <int KIND, int B>

@@ -70,6 +70,7 @@ class Solver {
     void upload(const double* host);    // replace level 0 from a host field
     void download(double* host);        // final field into a host buffer
     void kernel_stats(int which, double* seconds, long* launches, double* alg_bytes, double* updates) const;
+    void set_prof_kind(int k) { prof_kind_ = k; }
 
     const Setup& setup() const { return setup_; }
     double setup_seconds = 0.0;

@@ -456,7 +456,7 @@ SweptPlan compile_swept_plan(int b, const Equation& eq, long m, long final_level
                 if (!formula.count(kv.first)) fail(SG_ELOGIC, "plan: column exports miss a replayed read");
             P.overexport += static_cast<long>(formula.size() - exp_mask[kd].size());
             K.epad = static_cast<int>((K.exp_cells.size() + 3) / 4 * 4);
-            K.smem_doubles = std::max(1, col::imp_total(kd, b));
+            K.smem_doubles = std::max(1, col::imp_total(kd, b) + col::tile_doubles(kd, b));
             K.split = K.nlev;
             K.nexp_early = 0;
             P.max_epad = std::max(P.max_epad, K.epad);

@@ -42,11 +42,14 @@ def main():
                 t.append(s.solve())
             r = s.fetch()
             s.close()
-            p = sg.Solver(cfg, profile=True)
-            p.reset()
-            p.solve()
-            k = p.kernel_stats()
-            p.close()
+            kinds = {}
+            for name, kd in (("oct", 3), ("yb", 1), ("xb", 2)):
+                p = sg.Solver(cfg, profile=2 + kd)
+                p.reset()
+                p.solve()
+                kinds[name] = p.kernel_stats()
+                p.close()
+            k = kinds["oct"]
             same = None
             if ref is None:
                 ref = r.final_field.data
@@ -58,6 +61,8 @@ def main():
                               "dominant_launch_ms": 1e3 * k["seconds"] / max(1, k["launches"]),
                               "dominant_launches": k["launches"],
                               "dominant_alg_GBs": k["alg_bytes"] / max(k["seconds"], 1e-12) / 1e9,
+                              "yb_launch_ms": 1e3 * kinds["yb"]["seconds"] / max(1, kinds["yb"]["launches"]),
+                              "xb_launch_ms": 1e3 * kinds["xb"]["seconds"] / max(1, kinds["xb"]["launches"]),
                               "bitwise_equal_to_first": same}), flush=True)
 
 
