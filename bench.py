@@ -307,7 +307,7 @@ def main():
     achieved = per_launch_bytes / per_launch_s / 1e9
     tag = workload_config(n, nx, ny)["workload"]
     nt = ncu_traffic(tag)
-    roof = {"kernel": "swept_heat_kernel (Octahedron launches)", "bound": "hbm",
+    roof = {"kernel": "swept_heat_col_kernel<16, Octahedron> (register-tile Octahedron launches)", "bound": "hbm",
             "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": nt[0] if nt else None,
             "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else
@@ -326,6 +326,15 @@ def main():
         st.close()
         extra["standard"] = {"value": st_value, "unit": "cell-updates/s", "ms_per_step": 1e3 * st_dev / args.steps}
         extra["swept_over_standard"] = value / st_value
+        # the block-size axis (BASELINE configs[2]): b32 halves the swept bytes
+        # per update on the same grid; the standard engine does not depend on b
+        sb, sb_dev, sb_k, _ = timed("swept", False, block=32)
+        sb_rec = sb.fetch().record
+        sb.close()
+        extra["swept_b32"] = {"value": sb_rec.cell_updates * args.steps / sb_dev, "unit": "cell-updates/s",
+                              "actual_steps": sb_rec.actual_steps, "ms_per_step": 1e3 * sb_dev / args.steps,
+                              "swept_over_standard": (sb_rec.cell_updates * args.steps / sb_dev) /
+                              (st_rec.cell_updates / st_rec.actual_steps * sb_rec.actual_steps * args.steps / st_dev)}
         if n == 1:
             # configs[1]: Euler 960^2 b16 swept vs standard (one GPU)
             eu = {}

@@ -277,35 +277,38 @@ __device__ __noinline__ void put_cells(const SweptArgs& A, const double* stash, 
 }
 
 // Heat phase kernel, register-tile form (block B in {8, 16, 32}, geometry in
-// colgeom.hpp).  B lanes own one phase instance (32/B instances per warp, 4
-// warps per CTA).  At each level the instance's B x B window lives in the
-// lanes' registers, in one of two layouts (col::mode):
-//   COL: lane c holds column c, v[i] = row ylo + i;
-//   ROW: lane i holds row ylo + i, v[x] = column x.
+// colgeom.hpp).  L = B/CPL lanes own one phase instance (32/L instances per
+// warp, WPC warps per CTA).  At each level the instance's B x B window lives
+// in the lanes' registers, in one of two layouts (col::mode):
+//   COL: lane l holds columns c = CPL*l + q, v[q][i] = row ylo + i;
+//   ROW: lane l holds rows ylo + CPL*l + q, v[q][x] = column x.
 // The bridges switch layout once (a transpose through shared memory) so that
 // every level iterates over the shorter side of its rectangle.  Per level r
 // (geometry compile-time, levels and cells fully unrolled):
 //   1. imports: cells of level r-1 this instance did not compute come from
 //      shared memory, where the gather landed them (predicated LDS);
-//   2. update R_r in place: neighbours along the lane's own line are
-//      registers, across lines they come from lanes +-1 by warp shuffle
-//      (heat_point, physics.hpp:57-63; no FMA);
+//   2. update R_r in place: neighbours along a lane's lines and between its
+//      own CPL lines are registers; across lanes they come from lanes +-1 by
+//      warp shuffle, one 64-bit shuffle each way per CPL lines (heat_point,
+//      physics.hpp:57-63; no FMA);
 //   3. exports: the cells of R_r that other instances read go from registers
 //      into this instance's record (predicated stores).
 // Lanes outside R_r compute too (SIMT); their cells are never read before an
 // import overwrites them.
-template <int B, int KIND>
-__global__ void __launch_bounds__(128) swept_heat_col_kernel(const __grid_constant__ SweptArgs A) {
-    constexpr int IPW = 32 / B;
+template <int B, int KIND, int CPL, int WPC>
+__global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_constant__ SweptArgs A) {
+    constexpr int L = B / CPL;      // lanes per instance
+    constexpr int IPW = 32 / L;     // instances per warp
+    constexpr int IPC = WPC * IPW;  // instances per CTA
     constexpr int NL = col::nlev(KIND, B);
     constexpr int YLO = col::ylo(KIND, B);
     constexpr int NIMP = col::imp_total(KIND, B);  // import slots; the transpose tile follows
     extern __shared__ double sm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int sub = lane / B, l = lane % B;
+    const int sub = lane / L, l = lane % L;
     const int slot_in_cta = warp * IPW + sub;
     const int ninst = A.pbx * A.pby;
-    const int inst = blockIdx.x * (4 * IPW) + slot_in_cta;
+    const int inst = blockIdx.x * IPC + slot_in_cta;
     const bool live = inst < ninst;
     const int part = A.dev_parts[blockIdx.y];
     const int pi = part % A.px, pj = part / A.px;
@@ -318,19 +321,19 @@ __global__ void __launch_bounds__(128) swept_heat_col_kernel(const __grid_consta
     if (live) {
         const double* ibase = A.rec[part * A.nslots] + ((long)(bj + gh) * A.extw + (bi + gh)) * A.epad;
         int i = l;
-        for (; i + 3 * B < A.nimp; i += 4 * B) {
-            const int2 e0 = ldg_keep(&A.imp_off[i]), e1 = ldg_keep(&A.imp_off[i + B]);
-            const int2 e2 = ldg_keep(&A.imp_off[i + 2 * B]), e3 = ldg_keep(&A.imp_off[i + 3 * B]);
+        for (; i + 3 * L < A.nimp; i += 4 * L) {
+            const int2 e0 = ldg_keep(&A.imp_off[i]), e1 = ldg_keep(&A.imp_off[i + L]);
+            const int2 e2 = ldg_keep(&A.imp_off[i + 2 * L]), e3 = ldg_keep(&A.imp_off[i + 3 * L]);
             cp_async8(S + e0.y, ibase + e0.x);
             cp_async8(S + e1.y, ibase + e1.x);
             cp_async8(S + e2.y, ibase + e2.x);
             cp_async8(S + e3.y, ibase + e3.x);
         }
-        for (; i < A.nimp; i += B) {
+        for (; i < A.nimp; i += L) {
             const int2 e = ldg_keep(&A.imp_off[i]);
             cp_async8(S + e.y, ibase + e.x);
         }
-        for (int j = l; j < A.ninit; j += B) {
+        for (int j = l; j < A.ninit; j += L) {
             const int4 im = __ldg(&A.inits[j]);
             const int gx = wrapi(pi * A.pw + bi * B - half + im.x, A.nx);
             const int gy = wrapi(pj * A.ph + bj * B - half + im.y, A.ny);
@@ -346,123 +349,174 @@ __global__ void __launch_bounds__(128) swept_heat_col_kernel(const __grid_consta
     const unsigned s_imp = static_cast<unsigned>(__cvta_generic_to_shared(S));
     double* tile = S + NIMP;
     // output stash (only allocated by launches that write the output level or snapshots)
-    double* stash = sm + 4 * IPW * A.smem_doubles + (slot_in_cta * B + l) * B;
-    double v[B];
+    double* stash = sm + IPC * A.smem_doubles + (slot_in_cta * L + l) * CPL * B;
+    double v[CPL][B];
 #pragma unroll
-    for (int i = 0; i < B; ++i) v[i] = 0.0;
+    for (int q = 0; q < CPL; ++q)
+#pragma unroll
+        for (int i = 0; i < B; ++i) v[q][i] = 0.0;
 
     sfor<NL>([&](auto RI) {
         constexpr int r = decltype(RI)::value + 1;
         constexpr int MODE = col::mode(KIND, B, r);
-        constexpr col::CRect q = col::rect(KIND, B, r);
+        constexpr col::CRect q0 = col::rect(KIND, B, r);
         // ---------------- 1. imports of level r-1
         if constexpr (MODE == col::COL) {
-            bool ip[4];
-            unsigned ia[4];
+            bool ip[CPL][4];
+            unsigned ia[CPL][4];
             sfor<4>([&](auto TI) {
                 constexpr int t = decltype(TI)::value;
                 constexpr col::RowSet ts = col::Geo<KIND, B>::t.imp_tset[r][t];
-                ip[t] = ts.count() > 0 && ts.has(l);
-                ia[t] = s_imp + 8u * static_cast<unsigned>(ts.count() > 0 ? ts.rank(l) : 0);
+#pragma unroll
+                for (int q = 0; q < CPL; ++q) {
+                    const int c = CPL * l + q;
+                    ip[q][t] = ts.count() > 0 && ts.has(c);
+                    ia[q][t] = s_imp + 8u * static_cast<unsigned>(ts.count() > 0 ? ts.rank(c) : 0);
+                }
             });
             sfor<B>([&](auto YI) {
                 constexpr int j = decltype(YI)::value;
                 constexpr int t = col::Geo<KIND, B>::t.imp_type[r][j];
                 constexpr int base = col::Geo<KIND, B>::t.imp_base[r][j];
-                if constexpr (t >= 0) lds_if(v[j], ia[t] + 8u * base, ip[t]);
+                if constexpr (t >= 0) {
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) lds_if(v[q][j], ia[q][t] + 8u * base, ip[q][t]);
+                }
             });
         } else {
-            int myt = -1, mybase = 0;
-            sfor<col::kMaxRuns>([&](auto UI) {
-                constexpr col::Run ru = col::Geo<KIND, B>::t.imp_runs[r][decltype(UI)::value];
-                if constexpr (ru.t >= 0)
-                    if (l >= ru.i0 && l < ru.i1) {
-                        myt = ru.t;
-                        mybase = ru.base + (l - ru.i0) * ru.cnt;
-                    }
-            });
-            const unsigned ab = s_imp + 8u * static_cast<unsigned>(mybase);
+            int myt[CPL], mybase[CPL];
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) {
+                const int i = CPL * l + q;
+                myt[q] = -1;
+                mybase[q] = 0;
+                sfor<col::kMaxRuns>([&](auto UI) {
+                    constexpr col::Run ru = col::Geo<KIND, B>::t.imp_runs[r][decltype(UI)::value];
+                    if constexpr (ru.t >= 0)
+                        if (i >= ru.i0 && i < ru.i1) {
+                            myt[q] = ru.t;
+                            mybase[q] = ru.base + (i - ru.i0) * ru.cnt;
+                        }
+                });
+            }
             sfor<4>([&](auto TI) {
                 constexpr int t = decltype(TI)::value;
                 constexpr col::RowSet ts = col::Geo<KIND, B>::t.imp_tset[r][t];
                 if constexpr (ts.count() > 0) {
-                    const bool p = myt == t;
                     sfor<B>([&](auto XI) {
                         constexpr int x = decltype(XI)::value;
                         constexpr col::RowSet tx = col::Geo<KIND, B>::t.imp_tset[r][t];
                         constexpr int rk = tx.rank(x);
-                        if constexpr (tx.has(x)) lds_if(v[x], ab + 8u * rk, p);
+                        if constexpr (tx.has(x)) {
+#pragma unroll
+                            for (int q = 0; q < CPL; ++q)
+                                lds_if(v[q][x], s_imp + 8u * static_cast<unsigned>(mybase[q] + rk), myt[q] == t);
+                        }
                     });
                 }
             });
         }
         // ---------------- 2. update R_r in place
         if constexpr (MODE == col::COL) {
-            double prev = v[q.y0 - 1 - YLO];  // old value of the row below
+            double prev[CPL];  // old values of the row below
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) prev[q] = v[q][q0.y0 - 1 - YLO];
             sfor<B>([&](auto YI) {
                 constexpr int j = decltype(YI)::value;
                 constexpr col::CRect qr = col::rect(KIND, B, r);
                 if constexpr (YLO + j >= qr.y0 && YLO + j < qr.y1) {
-                    const double cur = v[j];
-                    const double e = __shfl_down_sync(0xffffffffu, cur, 1);
-                    const double w = __shfl_up_sync(0xffffffffu, cur, 1);
-                    v[j] = heat_update(cur, e, w, v[j + 1], prev, fx, fy);
-                    prev = cur;
+                    double cur[CPL];
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) cur[q] = v[q][j];
+                    const double east = __shfl_down_sync(0xffffffffu, cur[0], 1);
+                    const double west = __shfl_up_sync(0xffffffffu, cur[CPL - 1], 1);
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) {
+                        const double e = q + 1 < CPL ? cur[q + 1 < CPL ? q + 1 : 0] : east;
+                        const double w = q > 0 ? cur[q > 0 ? q - 1 : 0] : west;
+                        v[q][j] = heat_update(cur[q], e, w, v[q][j + 1], prev[q], fx, fy);
+                        prev[q] = cur[q];
+                    }
                 }
             });
         } else {
-            double prev = v[q.x0 - 1];  // old value of the column to the west
+            double prev[CPL];  // old values of the column to the west
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) prev[q] = v[q][q0.x0 - 1];
             sfor<B>([&](auto XI) {
                 constexpr int x = decltype(XI)::value;
                 constexpr col::CRect qr = col::rect(KIND, B, r);
                 if constexpr (x >= qr.x0 && x < qr.x1) {
-                    const double cur = v[x];
-                    const double n = __shfl_down_sync(0xffffffffu, cur, 1);
-                    const double s = __shfl_up_sync(0xffffffffu, cur, 1);
-                    v[x] = heat_update(cur, v[x + 1], prev, n, s, fx, fy);
-                    prev = cur;
+                    double cur[CPL];
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) cur[q] = v[q][x];
+                    const double north = __shfl_down_sync(0xffffffffu, cur[0], 1);
+                    const double south = __shfl_up_sync(0xffffffffu, cur[CPL - 1], 1);
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) {
+                        const double n = q + 1 < CPL ? cur[q + 1 < CPL ? q + 1 : 0] : north;
+                        const double sv = q > 0 ? cur[q > 0 ? q - 1 : 0] : south;
+                        v[q][x] = heat_update(cur[q], v[q][x + 1], prev[q], n, sv, fx, fy);
+                        prev[q] = cur[q];
+                    }
                 }
             });
         }
         // ---------------- 3. exports of level r
         if (live) {
             if constexpr (MODE == col::COL) {
-                bool ep[2];
-                double* eg[2];
+                bool ep[CPL][2];
+                double* eg[CPL][2];
                 sfor<2>([&](auto TI) {
                     constexpr int t = decltype(TI)::value;
                     constexpr col::RowSet ts = col::Geo<KIND, B>::t.exp_tset[r][t];
-                    ep[t] = ts.count() > 0 && ts.has(l);
-                    eg[t] = dst + (ts.count() > 0 ? ts.rank(l) : 0);
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) {
+                        const int c = CPL * l + q;
+                        ep[q][t] = ts.count() > 0 && ts.has(c);
+                        eg[q][t] = dst + (ts.count() > 0 ? ts.rank(c) : 0);
+                    }
                 });
                 sfor<B>([&](auto YI) {
                     constexpr int j = decltype(YI)::value;
                     constexpr int t = col::Geo<KIND, B>::t.exp_type[r][j];
-                    static_assert(t < 2, "export row types");
                     constexpr int base = col::Geo<KIND, B>::t.exp_base[r][j];
-                    if constexpr (t >= 0) stg_if(eg[t] + base, v[j], ep[t]);
+                    static_assert(t < 2, "export row types");
+                    if constexpr (t >= 0) {
+#pragma unroll
+                        for (int q = 0; q < CPL; ++q) stg_if(eg[q][t] + base, v[q][j], ep[q][t]);
+                    }
                 });
             } else {
-                int myt = -1, mybase = 0;
-                sfor<col::kMaxRuns>([&](auto UI) {
-                    constexpr col::Run ru = col::Geo<KIND, B>::t.exp_runs[r][decltype(UI)::value];
-                    if constexpr (ru.t >= 0)
-                        if (l >= ru.i0 && l < ru.i1) {
-                            myt = ru.t;
-                            mybase = ru.base + (l - ru.i0) * ru.cnt;
-                        }
-                });
-                double* eb = dst + mybase;
+                int myt[CPL];
+                double* eb[CPL];
+#pragma unroll
+                for (int q = 0; q < CPL; ++q) {
+                    const int i = CPL * l + q;
+                    myt[q] = -1;
+                    int mybase = 0;
+                    sfor<col::kMaxRuns>([&](auto UI) {
+                        constexpr col::Run ru = col::Geo<KIND, B>::t.exp_runs[r][decltype(UI)::value];
+                        if constexpr (ru.t >= 0)
+                            if (i >= ru.i0 && i < ru.i1) {
+                                myt[q] = ru.t;
+                                mybase = ru.base + (i - ru.i0) * ru.cnt;
+                            }
+                    });
+                    eb[q] = dst + mybase;
+                }
                 sfor<2>([&](auto TI) {
                     constexpr int t = decltype(TI)::value;
                     constexpr col::RowSet ts = col::Geo<KIND, B>::t.exp_tset[r][t];
                     if constexpr (ts.count() > 0) {
-                        const bool p = myt == t;
                         sfor<B>([&](auto XI) {
                             constexpr int x = decltype(XI)::value;
                             constexpr col::RowSet tx = col::Geo<KIND, B>::t.exp_tset[r][t];
                             constexpr int rk = tx.rank(x);
-                            if constexpr (tx.has(x)) stg_if(eb + rk, v[x], p);
+                            if constexpr (tx.has(x)) {
+#pragma unroll
+                                for (int q = 0; q < CPL; ++q) stg_if(eb[q] + rk, v[q][x], myt[q] == t);
+                            }
                         });
                     }
                 });
@@ -472,58 +526,74 @@ __global__ void __launch_bounds__(128) swept_heat_col_kernel(const __grid_consta
         // shared-memory stash to a non-inlined writer
         if (((A.out_mask | A.snap_mask) >> r) & 1ull) {
 #pragma unroll
-            for (int i = 0; i < B; ++i) stash[i] = v[i];
+            for (int q = 0; q < CPL; ++q)
+#pragma unroll
+                for (int i = 0; i < B; ++i) stash[q * B + i] = v[q][i];
             const long lev = A.lo + r - 1;
             const bool o = (A.out_mask >> r) & 1ull, sn = (A.snap_mask >> r) & 1ull;
-            if constexpr (MODE == col::COL) {
-                if (live && l >= q.x0 && l < q.x1)
-                    put_cells(A, stash, q.y0 - YLO, q.y1 - YLO, pi, pj, bi * B - half + l, bj * B - half + YLO, 0,
-                              1, lev, o, sn);
-            } else {
-                if (live && YLO + l >= q.y0 && YLO + l < q.y1)
-                    put_cells(A, stash, q.x0, q.x1, pi, pj, bi * B - half, bj * B - half + YLO + l, 1, 0, lev, o,
-                              sn);
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) {
+                const int m = CPL * l + q;  // the lane's column (COL) or window row (ROW)
+                if constexpr (MODE == col::COL) {
+                    if (live && m >= q0.x0 && m < q0.x1)
+                        put_cells(A, stash + q * B, q0.y0 - YLO, q0.y1 - YLO, pi, pj, bi * B - half + m,
+                                  bj * B - half + YLO, 0, 1, lev, o, sn);
+                } else {
+                    if (live && YLO + m >= q0.y0 && YLO + m < q0.y1)
+                        put_cells(A, stash + q * B, q0.x0, q0.x1, pi, pj, bi * B - half, bj * B - half + YLO + m, 1,
+                                  0, lev, o, sn);
+                }
             }
         }
         // ---------------- layout switch after this level: transpose R_r
         if constexpr (r < NL && col::mode(KIND, B, r + 1) != MODE) {
-            constexpr int w = q.x1 - q.x0;
-            static_assert(w * (q.y1 - q.y0) <= col::tile_doubles(KIND, B), "transpose tile");
-            if constexpr (MODE == col::COL) {
-                if (l >= q.x0 && l < q.x1) {
-                    double* t0 = tile + (l - q.x0);
-                    sfor<B>([&](auto YI) {
-                        constexpr int j = decltype(YI)::value;
-                        constexpr col::CRect qr = col::rect(KIND, B, r);
-                        if constexpr (YLO + j >= qr.y0 && YLO + j < qr.y1) t0[(YLO + j - qr.y0) * w] = v[j];
-                    });
+            constexpr int w = q0.x1 - q0.x0;
+            static_assert(w * (q0.y1 - q0.y0) <= col::tile_doubles(KIND, B), "transpose tile");
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) {
+                const int m = CPL * l + q;
+                if constexpr (MODE == col::COL) {
+                    if (m >= q0.x0 && m < q0.x1) {
+                        double* t0 = tile + (m - q0.x0);
+                        sfor<B>([&](auto YI) {
+                            constexpr int j = decltype(YI)::value;
+                            constexpr col::CRect qr = col::rect(KIND, B, r);
+                            if constexpr (YLO + j >= qr.y0 && YLO + j < qr.y1) t0[(YLO + j - qr.y0) * w] = v[q][j];
+                        });
+                    }
+                } else {
+                    if (YLO + m >= q0.y0 && YLO + m < q0.y1) {
+                        double* t0 = tile + (YLO + m - q0.y0) * w;
+                        sfor<B>([&](auto XI) {
+                            constexpr int x = decltype(XI)::value;
+                            constexpr col::CRect qr = col::rect(KIND, B, r);
+                            if constexpr (x >= qr.x0 && x < qr.x1) t0[x - qr.x0] = v[q][x];
+                        });
+                    }
                 }
-                __syncwarp();
-                if (YLO + l >= q.y0 && YLO + l < q.y1) {
-                    const double* t0 = tile + (YLO + l - q.y0) * w;
-                    sfor<B>([&](auto XI) {
-                        constexpr int x = decltype(XI)::value;
-                        constexpr col::CRect qr = col::rect(KIND, B, r);
-                        if constexpr (x >= qr.x0 && x < qr.x1) v[x] = t0[x - qr.x0];
-                    });
-                }
-            } else {
-                if (YLO + l >= q.y0 && YLO + l < q.y1) {
-                    double* t0 = tile + (YLO + l - q.y0) * w;
-                    sfor<B>([&](auto XI) {
-                        constexpr int x = decltype(XI)::value;
-                        constexpr col::CRect qr = col::rect(KIND, B, r);
-                        if constexpr (x >= qr.x0 && x < qr.x1) t0[x - qr.x0] = v[x];
-                    });
-                }
-                __syncwarp();
-                if (l >= q.x0 && l < q.x1) {
-                    const double* t0 = tile + (l - q.x0);
-                    sfor<B>([&](auto YI) {
-                        constexpr int j = decltype(YI)::value;
-                        constexpr col::CRect qr = col::rect(KIND, B, r);
-                        if constexpr (YLO + j >= qr.y0 && YLO + j < qr.y1) v[j] = t0[(YLO + j - qr.y0) * w];
-                    });
+            }
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) {
+                const int m = CPL * l + q;
+                if constexpr (MODE == col::COL) {  // now ROW: m = window row
+                    if (YLO + m >= q0.y0 && YLO + m < q0.y1) {
+                        const double* t0 = tile + (YLO + m - q0.y0) * w;
+                        sfor<B>([&](auto XI) {
+                            constexpr int x = decltype(XI)::value;
+                            constexpr col::CRect qr = col::rect(KIND, B, r);
+                            if constexpr (x >= qr.x0 && x < qr.x1) v[q][x] = t0[x - qr.x0];
+                        });
+                    }
+                } else {  // now COL: m = column
+                    if (m >= q0.x0 && m < q0.x1) {
+                        const double* t0 = tile + (m - q0.x0);
+                        sfor<B>([&](auto YI) {
+                            constexpr int j = decltype(YI)::value;
+                            constexpr col::CRect qr = col::rect(KIND, B, r);
+                            if constexpr (YLO + j >= qr.y0 && YLO + j < qr.y1) v[q][j] = t0[(YLO + j - qr.y0) * w];
+                        });
+                    }
                 }
             }
             __syncwarp();
@@ -534,9 +604,9 @@ __global__ void __launch_bounds__(128) swept_heat_col_kernel(const __grid_consta
     const bool edge = bi < gh || bi >= A.pbx - gh || bj < gh || bj >= A.pby - gh;
     if (edge && live && A.nexp > 0) {
         asm volatile("" ::: "memory");
-        if constexpr (B == 32) __syncwarp();
-        else __syncwarp(((1u << B) - 1u) << (sub * B));
-        for (int e = l; e < A.nexp; e += B) {
+        if constexpr (L == 32) __syncwarp();
+        else __syncwarp(((1u << L) - 1u) << (sub * L));
+        for (int e = l; e < A.nexp; e += L) {
             const double val = __ldcg(dst + e);
             for (int ej = -1; ej <= 1; ++ej)
                 for (int ei = -1; ei <= 1; ++ei) {
@@ -913,25 +983,32 @@ cudaError_t launch_dist_barrier(unsigned long long* const* peer_flags, unsigned 
     return cudaGetLastError();
 }
 
-template <int B>
-cudaError_t launch_heat_col(const SweptArgs& a, cudaStream_t s) {
-    constexpr int IPC = 4 * (32 / B);  // instances per CTA
+template <int B, int CPL, int WPC>
+cudaError_t launch_heat_col_t(const SweptArgs& a, cudaStream_t s) {
+    constexpr int IPC = WPC * (32 / (B / CPL));  // instances per CTA
     const bool stash = (a.out_mask | a.snap_mask) != 0ull;
     const size_t smem = static_cast<size_t>(IPC) * (a.smem_doubles + (stash ? B * B : 0)) * sizeof(double);
     const int ninst = a.pbx * a.pby;
     dim3 grid((ninst + IPC - 1) / IPC, a.ndev_parts);
     auto go = [&](auto kern) {
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<grid, 128, smem, s>>>(a);
+        kern<<<grid, WPC * 32, smem, s>>>(a);
         return cudaGetLastError();
     };
     switch (a.kind) {
-        case col::UP: return go(swept_heat_col_kernel<B, col::UP>);
-        case col::YB: return go(swept_heat_col_kernel<B, col::YB>);
-        case col::XB: return go(swept_heat_col_kernel<B, col::XB>);
-        case col::OCT: return go(swept_heat_col_kernel<B, col::OCT>);
-        default: return go(swept_heat_col_kernel<B, col::DOWN>);
+        case col::UP: return go(swept_heat_col_kernel<B, col::UP, CPL, WPC>);
+        case col::YB: return go(swept_heat_col_kernel<B, col::YB, CPL, WPC>);
+        case col::XB: return go(swept_heat_col_kernel<B, col::XB, CPL, WPC>);
+        case col::OCT: return go(swept_heat_col_kernel<B, col::OCT, CPL, WPC>);
+        default: return go(swept_heat_col_kernel<B, col::DOWN, CPL, WPC>);
     }
+}
+// One column (row) per lane: two per lane halves the shuffles but doubles the
+// live registers (Oct b16: 182 vs 106), and the lost occupancy costs more
+// (Oct launch 0.82 vs 0.62 ms, profiles/r01_summary.md).
+template <int B>
+cudaError_t launch_heat_col(const SweptArgs& a, cudaStream_t s) {
+    return launch_heat_col_t<B, 1, 4>(a, s);
 }
 
 cudaError_t launch_swept(int problem, const SweptArgs& a, cudaStream_t s) {
