@@ -986,9 +986,9 @@ cudaError_t launch_dist_barrier(unsigned long long* const* peer_flags, unsigned 
 template <int B, int CPL, int WPC>
 cudaError_t launch_heat_col_t(const SweptArgs& a, cudaStream_t s) {
     constexpr int IPC = WPC * (32 / (B / CPL));  // instances per CTA
+    const int ninst = a.pbx * a.pby;
     const bool stash = (a.out_mask | a.snap_mask) != 0ull;
     const size_t smem = static_cast<size_t>(IPC) * (a.smem_doubles + (stash ? B * B : 0)) * sizeof(double);
-    const int ninst = a.pbx * a.pby;
     dim3 grid((ninst + IPC - 1) / IPC, a.ndev_parts);
     auto go = [&](auto kern) {
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1008,6 +1008,10 @@ cudaError_t launch_heat_col_t(const SweptArgs& a, cudaStream_t s) {
 // (Oct launch 0.82 vs 0.62 ms, profiles/r01_summary.md).
 template <int B>
 cudaError_t launch_heat_col(const SweptArgs& a, cudaStream_t s) {
+    // 4 warps per CTA on big grids; single-warp CTAs when there are too few
+    // instances to fill the 148 SMs otherwise (the paper's 320^2..1120^2 grids)
+    if constexpr (B == 16)
+        if (a.pbx * a.pby * a.ndev_parts < 2 * 4 * 148 * 8) return launch_heat_col_t<B, 1, 1>(a, s);
     return launch_heat_col_t<B, 1, 4>(a, s);
 }
 
