@@ -1,0 +1,50 @@
+"""Register-tile (column/row lane) heat kernels, colgeom.hpp + kernels.cu
+swept_heat_col_kernel: bitwise equal to the generic table-driven kernels and
+to the CPU oracle over many swept cycles, for every supported block size,
+with partitions (edge instances push their records into neighbours' ghost
+rings) and with the output level falling inside each phase kind."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _need_gpu(sg):
+    if sg.device_count() < 1:
+        pytest.fail("no CUDA device visible: the -m gpu suite must run on a B200")
+
+
+def _oracle_final(oracle, nx, ny, levels):
+    init, params = oracle.params(oracle.HEAT, nx, ny)
+    return oracle.standard_solve(oracle.HEAT, init, levels, params)
+
+
+def _solve(sg, monkeypatch, kernel, **kw):
+    monkeypatch.setenv("SG_HEAT_KERNEL", kernel)
+    return sg.run(sg.SolverConfig(problem="heat", **kw))
+
+
+@pytest.mark.parametrize("block,nx,steps", [(8, 128, 97), (16, 256, 190), (32, 512, 200)])
+def test_column_matches_generic_and_oracle(sg, oracle, monkeypatch, block, nx, steps):
+    _need_gpu(sg)
+    col = _solve(sg, monkeypatch, "column", nx=nx, block=block, steps=steps)
+    gen = _solve(sg, monkeypatch, "generic", nx=nx, block=block, steps=steps)
+    assert col.record.kernel_launches == gen.record.kernel_launches
+    assert np.array_equal(col.final_field.data, gen.final_field.data)
+    assert np.array_equal(col.final_field.data, _oracle_final(oracle, nx, nx, col.final_field.level))
+
+
+@pytest.mark.parametrize("block,nx,ny,px,py", [(32, 256, 256, 2, 2), (8, 128, 64, 2, 1), (16, 192, 384, 3, 2)])
+def test_column_partitions(sg, oracle, monkeypatch, block, nx, ny, px, py):
+    _need_gpu(sg)
+    res = _solve(sg, monkeypatch, "column", nx=nx, ny=ny, block=block, steps=61, ranks=px * py, px=px, py=py)
+    assert np.array_equal(res.final_field.data, _oracle_final(oracle, nx, ny, res.final_field.level))
+
+
+@pytest.mark.parametrize("steps", [3, 7, 9, 12, 17, 22])
+def test_column_output_level_in_every_phase(sg, oracle, monkeypatch, steps):
+    """b16 (k = 7): the final level lands in UpPyramid, an XBridge / YBridge /
+    Octahedron launch or the DownPyramid depending on the step count."""
+    _need_gpu(sg)
+    res = _solve(sg, monkeypatch, "column", nx=64, block=16, steps=steps)
+    assert np.array_equal(res.final_field.data, _oracle_final(oracle, 64, 64, res.final_field.level))

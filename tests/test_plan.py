@@ -79,3 +79,17 @@ def test_swept_traffic_per_update_table(sg, b, expect):
     byt = 8 * (d["oct_imports"] + d["oct_exports"] + 2 * (d["yb_imports"] + d["yb_exports"]))
     upd = d["oct_updates"] + 2 * d["yb_updates"]
     assert byt / upd == pytest.approx(expect, abs=0.01)
+
+
+@pytest.mark.parametrize("b", [8, 16, 32])
+def test_column_layout_covers_the_replayed_reads_exactly(sg, b):
+    """The closed-form import/export sets of the register-tile kernels
+    (colgeom.hpp) cover every cross-instance read of the schedule replay and,
+    in the steady state, nothing more (overexport = 0)."""
+    d = sg.plan_info("heat", b, 40 * b)
+    assert "heat_kernel=column" in d["text"] and "overexport=0" in d["text"]
+
+
+def test_generic_kernels_for_other_blocks(sg):
+    assert "heat_kernel=generic" in sg.plan_info("heat", 12, 200)["text"]
+    assert "heat_kernel=generic" in sg.plan_info("euler", 16, 200)["text"]
