@@ -123,7 +123,7 @@ void spread_banks(std::vector<T>& v, std::size_t begin, std::size_t end, Key key
     }
 }
 
-SweptPlan compile_swept_plan(int b, const Equation& eq, long m, long final_level) {
+SweptPlan compile_swept_plan(int b, const Equation& eq, long m, long final_level, long instances) {
     SweptPlan P;
     P.b = b;
     P.n = eq.halo;
@@ -136,7 +136,8 @@ SweptPlan compile_swept_plan(int b, const Equation& eq, long m, long final_level
     const int n = P.n, k = P.k, S = P.S;
     {
         const char* env = std::getenv("SG_HEAT_KERNEL");
-        const bool generic = env && std::strcmp(env, "generic") == 0;
+        const bool forced = env && std::strcmp(env, "column") == 0;
+        const bool generic = (env && std::strcmp(env, "generic") == 0) || (!forced && instances > 0 && instances < 2048);
         if (eq.problem == SG_HEAT && n == 1 && S == 1 && col::supported(b) && !generic) P.colB = b;
     }
     if (final_level < 1 || final_level > P.flat) fail(SG_ELOGIC, "plan: final level outside the schedule");

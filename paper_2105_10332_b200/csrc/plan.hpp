@@ -122,10 +122,13 @@ void lane_split(int w, int h, int* splits, int* rps);
 template <class T, class Key>
 void spread_banks(std::vector<T>& v, std::size_t begin, std::size_t end, Key key);
 
-// m = octahedra; final_level = the level the run must output.  Heat runs with
-// b in {8, 16, 32} use the column-register kernels (colgeom.hpp) unless
-// SG_HEAT_KERNEL=generic is set in the environment.
-SweptPlan compile_swept_plan(int b, const Equation& eq, long m, long final_level);
+// m = octahedra; final_level = the level the run must output; instances =
+// block instances per launch over all partitions (0: unknown).  Heat runs with
+// b in {8, 16, 32} use the register-tile kernels (colgeom.hpp) unless
+// SG_HEAT_KERNEL=generic is set, or the grid is so small (< 2048 instances)
+// that the per-instance latency of the generic kernels wins (SG_HEAT_KERNEL=
+// column forces them).
+SweptPlan compile_swept_plan(int b, const Equation& eq, long m, long final_level, long instances = 0);
 
 std::string describe_plan(const SweptPlan& p);
 

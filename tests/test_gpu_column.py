@@ -46,5 +46,5 @@ def test_column_output_level_in_every_phase(sg, oracle, monkeypatch, steps):
     """b16 (k = 7): the final level lands in UpPyramid, an XBridge / YBridge /
     Octahedron launch or the DownPyramid depending on the step count."""
     _need_gpu(sg)
-    res = _solve(sg, monkeypatch, "column", nx=64, block=16, steps=steps)
+    res = _solve(sg, monkeypatch, "column", nx=64, block=16, steps=steps)  # forced: 16 instances
     assert np.array_equal(res.final_field.data, _oracle_final(oracle, 64, 64, res.final_field.level))
