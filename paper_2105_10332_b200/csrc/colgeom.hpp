@@ -275,6 +275,18 @@ struct Geo {
     static constexpr Tables t = make_tables(KIND, B);
 };
 
+// Two-part gather: imports read by levels <= gather_split (part A) are waited
+// for before level 1, the rest (part B) only before level split+1, so part
+// B's HBM latency overlaps the first levels' compute.
+SG_HD constexpr int last_imp_level(int kind, int B) {
+    int last = 0;
+    for (int r = 1; r <= nlev(kind, B); ++r)
+        for (int y = ylo(kind, B); y < ylo(kind, B) + B; ++y)
+            if (imp_row(kind, B, r, y).count() > 0) last = r;
+    return last;
+}
+SG_HD constexpr int gather_split(int kind, int B) { return (last_imp_level(kind, B) + 1) / 2; }
+
 SG_HD constexpr bool supported(int B) { return B == 8 || B == 16 || B == 32; }
 
 }  // namespace col

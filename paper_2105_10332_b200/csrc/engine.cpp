@@ -272,12 +272,6 @@ void Solver::finalize_swept() {
                 im2.push_back(make_int2((x.seg << 20) | x.src, x.dst));
             }
             d.d_imp2.push_back(dev_upload(d, im2));
-            std::vector<unsigned> pk;
-            for (const Import& x : T.imports) {
-                if (x.src >= (1 << 16) || x.dst >= (1 << 16)) fail(SG_ELOGIC, "swept: packed import table overflow");
-                pk.push_back((static_cast<unsigned>(x.src) << 16) | static_cast<unsigned>(x.dst));
-            }
-            d.d_imp_packed.push_back(dev_upload(d, pk));
             for (const InitImport& x : T.inits) in.push_back(make_int4(x.rx, x.ry, x.dst, x.vstride));
             d.d_imp.push_back(dev_upload(d, im));
             d.d_init.push_back(dev_upload(d, in));
@@ -329,7 +323,6 @@ void Solver::finalize_swept() {
             a.pitch = d.d_pitch[L.kind];
             a.imports = d.d_imp[L.cls];
             a.imports2 = d.d_imp2[L.cls];
-            a.imp_packed = d.d_imp_packed[L.cls];
             if (P.colB) {
                 // imports as signed offsets from the consumer instance's slot-0
                 // record base: producer slot * rec_len + (dj*extw + di)*stride + src
@@ -351,22 +344,14 @@ void Solver::finalize_swept() {
                 a.imp_off = it->second;
             }
             a.nimp = static_cast<int>(T.imports.size());
+            a.nimp_b = T.nimp_b;
             a.inits = d.d_init[L.cls];
             a.ninit = static_cast<int>(T.inits.size());
             if (T.segs.size() > static_cast<std::size_t>(kMaxSegs)) fail(SG_ELOGIC, "swept: too many segments");
             for (std::size_t s = 0; s < T.segs.size(); ++s) {
                 const long pl = static_cast<long>(li) - T.segs[s].delta;
                 if (pl < 0 || P.launches[pl].slot < 0) fail(SG_ELOGIC, "swept: import from a launch without record");
-                int beg = static_cast<int>(T.imports.size()), end = 0;
-                for (std::size_t q = 0; q < T.imports.size(); ++q)
-                    if (T.imports[q].seg == static_cast<int>(s)) {
-                        beg = std::min(beg, static_cast<int>(q));
-                        end = std::max(end, static_cast<int>(q) + 1);
-                    }
-                if (beg > end) beg = end = 0;
-                for (int q = beg; P.colB && q < end; ++q)
-                    if (T.imports[q].seg != static_cast<int>(s)) fail(SG_ELOGIC, "swept: import segment not contiguous");
-                a.segs[s] = {P.launches[pl].slot, T.segs[s].di, T.segs[s].dj, P.max_epad, beg, end};
+                a.segs[s] = {P.launches[pl].slot, T.segs[s].di, T.segs[s].dj, P.max_epad};
             }
             a.nsegs = static_cast<int>(T.segs.size());
             a.frame = L.frame;

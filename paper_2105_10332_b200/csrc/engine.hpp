@@ -46,7 +46,6 @@ struct DeviceCtx {
     int2* d_pitch[K_NKINDS] = {};
     std::vector<int4*> d_imp, d_init;
     std::vector<int2*> d_imp2;
-    std::vector<unsigned*> d_imp_packed;
     std::map<std::pair<int, int>, int2*> imp_off;  // (class, slot rotation) -> column gather table
     double** d_rec_tab = nullptr;
     double** d_frames_tab = nullptr;

@@ -67,6 +67,11 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
     const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // Heat phase kernel: one WARP per block instance, WPC instances per CTA, no
@@ -320,7 +325,23 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
     // ---- gather the imports: {offset from this instance's slot-0 record, smem slot}
     if (live) {
         const double* ibase = A.rec[part * A.nslots] + ((long)(bj + gh) * A.extw + (bi + gh)) * A.epad;
+        // part A (levels <= gather_split), one cp.async group, then part B
+        const int na = A.nimp - A.nimp_b;
         int i = l;
+        for (; i + 3 * L < na; i += 4 * L) {
+            const int2 e0 = ldg_keep(&A.imp_off[i]), e1 = ldg_keep(&A.imp_off[i + L]);
+            const int2 e2 = ldg_keep(&A.imp_off[i + 2 * L]), e3 = ldg_keep(&A.imp_off[i + 3 * L]);
+            cp_async8(S + e0.y, ibase + e0.x);
+            cp_async8(S + e1.y, ibase + e1.x);
+            cp_async8(S + e2.y, ibase + e2.x);
+            cp_async8(S + e3.y, ibase + e3.x);
+        }
+        for (; i < na; i += L) {
+            const int2 e = ldg_keep(&A.imp_off[i]);
+            cp_async8(S + e.y, ibase + e.x);
+        }
+        cp_async_commit();
+        i = na + l;
         for (; i + 3 * L < A.nimp; i += 4 * L) {
             const int2 e0 = ldg_keep(&A.imp_off[i]), e1 = ldg_keep(&A.imp_off[i + L]);
             const int2 e2 = ldg_keep(&A.imp_off[i + 2 * L]), e3 = ldg_keep(&A.imp_off[i + 3 * L]);
@@ -341,7 +362,8 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
             S[im.z] = A.init_planes[opj * A.px + opi][(long)(gy - opj * A.ph) * A.pw + (gx - opi * A.pw)];
         }
     }
-    cp_async_wait_all();
+    cp_async_commit();
+    cp_async_wait_group<1>();  // part A (part B may still be in flight)
     __syncwarp();
 
     double* dst = A.rec[part * A.nslots + A.my_slot] + ((long)(bj + gh) * A.extw + (bi + gh)) * A.epad;
@@ -360,6 +382,10 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
         constexpr int r = decltype(RI)::value + 1;
         constexpr int MODE = col::mode(KIND, B, r);
         constexpr col::CRect q0 = col::rect(KIND, B, r);
+        if constexpr (r == col::gather_split(KIND, B) + 1) {
+            cp_async_wait_all();  // part B
+            __syncwarp();
+        }
         // ---------------- 1. imports of level r-1
         if constexpr (MODE == col::COL) {
             bool ip[CPL][4];

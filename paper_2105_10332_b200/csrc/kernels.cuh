@@ -19,7 +19,6 @@ struct DevSeg {
     int slot;   // record slot of the producer launch
     int di, dj;
     int epad;   // producer record length
-    int beg, end;  // column kernels: this segment's entries of imp_packed
 };
 
 // Uniform per-level parameters of the heat phase kernel, kept in the kernel's
@@ -46,8 +45,8 @@ struct SweptArgs {
     // class tables
     const int4* imports;     // {seg, src, dst, vstride}
     const int2* imports2;    // {seg << 20 | src, dst}  (same entries, compact)
-    const unsigned* imp_packed;  // column kernels: src << 16 | dst, grouped by segment
     const int2* imp_off;     // column kernels: {offset from the instance's slot-0 record, smem slot}
+    int nimp_b;              // column kernels: the last nimp_b entries are gather part B
     int nimp;
     const int4* inits;       // {rx, ry, dst, vstride}
     int ninit;

@@ -513,8 +513,17 @@ SweptPlan compile_swept_plan(int b, const Equation& eq, long m, long final_level
         std::sort(T.imports.begin(), T.imports.end(), [](const Import& a, const Import& c) {
             return std::tie(a.seg, a.src) < std::tie(c.seg, c.src);
         });
-        // column kernels gather segment by segment: keep the (seg, src) order
-        if (!P.colB) spread_banks(T.imports, 0, T.imports.size(), [](const Import& e) { return e.dst; });
+        if (P.colB) {
+            // column kernels: part A (levels <= gather_split) before part B,
+            // each in (seg, src) order
+            const int split = col::gather_split(T.kind, b);
+            std::stable_sort(T.imports.begin(), T.imports.end(), [split](const Import& a, const Import& c) {
+                return (a.r + 1 > split) < (c.r + 1 > split);
+            });
+            for (const Import& x : T.imports) T.nimp_b += x.r + 1 > split ? 1 : 0;
+        } else {
+            spread_banks(T.imports, 0, T.imports.size(), [](const Import& e) { return e.dst; });
+        }
         if (P.colB) {
             std::vector<int> seen(static_cast<std::size_t>(K.smem_doubles), 0);
             for (const Import& x : T.imports) seen.at(static_cast<std::size_t>(x.dst))++;

@@ -79,7 +79,8 @@ struct InitImport {       // a level-0 cell read straight from the initial plane
 struct ClassTab {
     int kind = 0;
     std::vector<Segment> segs;
-    std::vector<Import> imports;       // sorted by (seg, src)
+    std::vector<Import> imports;       // sorted by (seg, src); column kernels: (part, seg, src)
+    int nimp_b = 0;                    // column kernels: imports of levels > gather_split (part B)
     std::vector<InitImport> inits;
 };
 
