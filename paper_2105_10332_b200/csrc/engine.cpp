@@ -345,6 +345,7 @@ void Solver::finalize_swept() {
             }
             a.nimp = static_cast<int>(T.imports.size());
             a.nimp_b = T.nimp_b;
+            a.lo_parity = std::getenv("SG_NO_SERPENTINE") ? 0 : static_cast<int>(li & 1);
             a.inits = d.d_init[L.cls];
             a.ninit = static_cast<int>(T.inits.size());
             if (T.segs.size() > static_cast<std::size_t>(kMaxSegs)) fail(SG_ELOGIC, "swept: too many segments");

@@ -313,7 +313,10 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
     const int sub = lane / L, l = lane % L;
     const int slot_in_cta = warp * IPW + sub;
     const int ninst = A.pbx * A.pby;
-    const int inst = blockIdx.x * IPC + slot_in_cta;
+    // odd launches walk the instances backwards: their first CTAs read the
+    // records the previous launch wrote last (still in L2)
+    const int cta = (A.lo_parity & 1) ? gridDim.x - 1 - blockIdx.x : blockIdx.x;
+    const int inst = cta * IPC + slot_in_cta;
     const bool live = inst < ninst;
     const int part = A.dev_parts[blockIdx.y];
     const int pi = part % A.px, pj = part / A.px;

@@ -47,6 +47,7 @@ struct SweptArgs {
     const int2* imports2;    // {seg << 20 | src, dst}  (same entries, compact)
     const int2* imp_off;     // column kernels: {offset from the instance's slot-0 record, smem slot}
     int nimp_b;              // column kernels: the last nimp_b entries are gather part B
+    int lo_parity;           // column kernels: launch index parity (odd: CTAs walk the instances backwards)
     int nimp;
     const int4* inits;       // {rx, ry, dst, vstride}
     int ninit;
