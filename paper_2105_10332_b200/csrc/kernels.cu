@@ -1041,6 +1041,9 @@ cudaError_t launch_heat_col(const SweptArgs& a, cudaStream_t s) {
     // instances to fill the 148 SMs otherwise (the paper's 320^2..1120^2 grids)
     if constexpr (B == 16)
         if (a.pbx * a.pby * a.ndev_parts < 2 * 4 * 148 * 8) return launch_heat_col_t<B, 1, 1>(a, s);
+    // b16: 2-warp CTAs (finer-grained residency: 18 instead of 16 warps per
+    // SM at ~100 registers; 3.69e11 vs 3.65e11 (4 warps) and 3.61e11 (8))
+    if constexpr (B == 16) return launch_heat_col_t<B, 1, 2>(a, s);
     return launch_heat_col_t<B, 1, 4>(a, s);
 }
 
