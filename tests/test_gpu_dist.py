@@ -43,11 +43,17 @@ def _worker(rank, world, port, cfgd, q):
 
 
 @pytest.mark.timeout(600)
-@pytest.mark.parametrize("engine", ["swept", "standard"])
+@pytest.mark.parametrize("engine,kernel", [("swept", "generic"), ("swept", "column"), ("standard", "generic")])
 @pytest.mark.parametrize("problem,px,py", [("heat", 2, 1), ("heat", 1, 2), ("euler", 2, 1)])
-def test_two_process_partitions_bitwise(sg, oracle, engine, problem, px, py):
+def test_two_process_partitions_bitwise(sg, oracle, monkeypatch, engine, kernel, problem, px, py):
+    """kernel: the swept heat phase kernels (SG_HEAT_KERNEL, inherited by the
+    spawned ranks); "column" = the register-tile kernels, whose partition-edge
+    instances push their records into the other rank's ghost ring."""
     if sg.device_count() < 1:
         pytest.fail("no CUDA device")
+    if kernel == "column" and problem != "heat":
+        pytest.skip("register-tile kernels are heat-only")
+    monkeypatch.setenv("SG_HEAT_KERNEL", kernel)
     import torch.multiprocessing as mp
     nx = 64
     cfgd = dict(problem=problem, nx=nx, block=16 if problem == "heat" else 8, steps=12, engine=engine,
