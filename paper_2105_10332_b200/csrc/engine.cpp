@@ -152,6 +152,8 @@ Solver::~Solver() {
         for (void* p : ipc_open_) cudaIpcCloseMemHandle(p);
         ipc_open_.clear();
         for (auto e : d.prof_ev) cudaEventDestroy(e);
+        for (auto e : d.launch_ev) cudaEventDestroy(e);
+        if (d.side) cudaStreamDestroy(d.side);
         cudaEventDestroy(d.ev_start);
         cudaEventDestroy(d.ev_stop);
         cudaEventDestroy(d.ev_sync);
@@ -574,10 +576,65 @@ double Solver::solve() {
         writer = std::make_unique<SnapshotWriter>(snap_path_, m);
         writer->append_frame(0, setup_.initial.data());  // level 0 % every == 0
     }
+    // Single device, no profiling / snapshots: an XBridge launch that does not
+    // depend on the YBridge launched just before it (the XBridge reads only the
+    // previous cycle's YBridge) runs on a second stream, so the
+    // two bridges of a cycle overlap (their launch tails and gather ramps).
+    // Cross-stream edges come from the plan: producer launches (segments),
+    // earlier readers of the record slot a launch overwrites, and its previous
+    // writer.
+    const bool concurrent = cfg_.engine == SG_SWEPT && !multi && !dist() && !writer && !profile &&
+                            !std::getenv("SG_SERIAL_BRIDGES");
+    std::vector<int> on_side;
+    if (concurrent) {
+        DeviceCtx& d = d0;
+        if (!d.side) ck(cudaStreamCreateWithFlags(&d.side, cudaStreamNonBlocking), "stream");
+        while (d.launch_ev.size() < plan_.launches.size()) {
+            cudaEvent_t e;
+            ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+            d.launch_ev.push_back(e);
+        }
+        on_side.assign(plan_.launches.size(), 0);
+    }
+    auto deps_of = [&](std::size_t li) {
+        std::vector<long> deps;
+        const long n = plan_.nslots;
+        const long L = static_cast<long>(li);
+        for (const Segment& sg : plan_.classes[plan_.launches[li].cls].segs) deps.push_back(L - sg.delta);
+        if (plan_.launches[li].slot >= 0) {
+            deps.push_back(L - n);  // previous writer of this slot
+            for (long q = std::max(0L, L - n + 1); q < L; ++q)  // its readers
+                for (const Segment& sg : plan_.classes[plan_.launches[q].cls].segs)
+                    if (q - sg.delta == L - n) deps.push_back(q);
+        }
+        return deps;
+    };
     auto enqueue = [&]() {
         if (cfg_.engine == SG_SWEPT) {
+            cudaEvent_t fork = nullptr;
+            if (concurrent) {  // bring the side stream into the capture / stream order
+                fork = d0.launch_ev[0];
+                ck(cudaEventRecord(fork, d0.stream), "event");
+                ck(cudaStreamWaitEvent(d0.side, fork, 0), "wait");
+            }
+            long last_side = -1;
             for (std::size_t li = 0; li < plan_.launches.size(); ++li) {
                 const bool pr = profile && plan_.launches[li].kind == prof_kind_;
+                if (concurrent) {
+                    const std::vector<long> deps = deps_of(li);
+                    const bool side = li > 0 && plan_.launches[li].kind == K_XB &&
+                                      plan_.launches[li - 1].kind == K_YB &&
+                                      std::find(deps.begin(), deps.end(), static_cast<long>(li) - 1) == deps.end();
+                    on_side[li] = side;
+                    cudaStream_t st = side ? d0.side : d0.stream;
+                    for (long q : deps)
+                        if (q >= 0 && on_side[q] != static_cast<int>(side)) ck(cudaStreamWaitEvent(st, d0.launch_ev[q], 0), "wait");
+                    ck(launch_swept(prob, d0.swept_args[li], st), "swept launch");
+                    ck(cudaEventRecord(d0.launch_ev[li], st), "event");
+                    ++launches_;
+                    if (side) last_side = static_cast<long>(li);
+                    continue;
+                }
                 for (auto& d : devs_) {
                     if (multi) cudaSetDevice(d.dev);
                     if (&d == &d0) prof_begin(pr);
@@ -599,6 +656,13 @@ double Solver::solve() {
                 if (writer)
                     for (long l : done_after_[li])
                         if (l % snap_every_ == 0) snapshot_frame(*writer, l, static_cast<int>(l % frame_ring_));
+            }
+            if (concurrent) {  // join: the main stream waits for the side stream's last launch
+                if (last_side >= 0) ck(cudaStreamWaitEvent(d0.stream, d0.launch_ev[last_side], 0), "wait");
+                else {
+                    ck(cudaEventRecord(fork, d0.side), "event");
+                    ck(cudaStreamWaitEvent(d0.stream, fork, 0), "wait");
+                }
             }
         } else {
             const Equation& eq = setup_.eq;

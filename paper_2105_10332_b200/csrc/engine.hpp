@@ -56,6 +56,9 @@ struct DeviceCtx {
     // per-launch arguments (swept) -- built once at create
     std::vector<SweptArgs> swept_args;
     std::vector<cudaEvent_t> prof_ev;   // kernel profiling pairs
+    // concurrent bridges (single device): a second stream and one event per launch
+    cudaStream_t side = nullptr;
+    std::vector<cudaEvent_t> launch_ev;
 };
 
 class Solver {
