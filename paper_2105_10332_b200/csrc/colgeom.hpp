@@ -3,7 +3,7 @@
 // every imported cell lands in shared memory and where every exported cell
 // sits in an instance's record.
 //
-// Column mode (heat, n = 1, S = 1, block B in {8, 16, 32}): B lanes own one
+// Column mode (heat, n = 1, S = 1, block B in {8, 12, 16, 24, 32}): B lanes own one
 // phase instance, lane c = instance column c, and each lane holds its
 // column's cells of the current level in registers, rows [ylo, ylo + B).
 // Every kind's cells (computed and read) fit that B x B window:
@@ -287,7 +287,7 @@ SG_HD constexpr int last_imp_level(int kind, int B) {
 }
 SG_HD constexpr int gather_split(int kind, int B) { return (last_imp_level(kind, B) + 1) / 2; }
 
-SG_HD constexpr bool supported(int B) { return B == 8 || B == 16 || B == 32; }
+SG_HD constexpr bool supported(int B) { return B == 8 || B == 12 || B == 16 || B == 24 || B == 32; }
 
 }  // namespace col
 }  // namespace sg

@@ -310,14 +310,17 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
     constexpr int NIMP = col::imp_total(KIND, B);  // import slots; the transpose tile follows
     extern __shared__ double sm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int sub = lane / L, l = lane % L;
+    // b = 12 / 24: the last 32 - IPW*L lanes of a warp are dead (they run the
+    // code, shuffles included, but never write anything)
+    const bool dead = lane >= IPW * L;
+    const int sub = dead ? 0 : lane / L, l = lane % L;
     const int slot_in_cta = warp * IPW + sub;
     const int ninst = A.pbx * A.pby;
     // odd launches walk the instances backwards: their first CTAs read the
     // records the previous launch wrote last (still in L2)
     const int cta = (A.lo_parity & 1) ? gridDim.x - 1 - blockIdx.x : blockIdx.x;
     const int inst = cta * IPC + slot_in_cta;
-    const bool live = inst < ninst;
+    const bool live = !dead && inst < ninst;
     const int part = A.dev_parts[blockIdx.y];
     const int pi = part % A.px, pj = part / A.px;
     const int bi = live ? inst % A.pbx : 0, bj = live ? inst / A.pbx : 0;
@@ -553,7 +556,7 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
         }
         // ---------------- output level / snapshot (rare): through the lane's
         // shared-memory stash to a non-inlined writer
-        if (((A.out_mask | A.snap_mask) >> r) & 1ull) {
+        if ((((A.out_mask | A.snap_mask) >> r) & 1ull) && !dead) {
 #pragma unroll
             for (int q = 0; q < CPL; ++q)
 #pragma unroll
@@ -582,7 +585,7 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
             for (int q = 0; q < CPL; ++q) {
                 const int m = CPL * l + q;
                 if constexpr (MODE == col::COL) {
-                    if (m >= q0.x0 && m < q0.x1) {
+                    if (!dead && m >= q0.x0 && m < q0.x1) {
                         double* t0 = tile + (m - q0.x0);
                         sfor<B>([&](auto YI) {
                             constexpr int j = decltype(YI)::value;
@@ -591,7 +594,7 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
                         });
                     }
                 } else {
-                    if (YLO + m >= q0.y0 && YLO + m < q0.y1) {
+                    if (!dead && YLO + m >= q0.y0 && YLO + m < q0.y1) {
                         double* t0 = tile + (YLO + m - q0.y0) * w;
                         sfor<B>([&](auto XI) {
                             constexpr int x = decltype(XI)::value;
@@ -1052,6 +1055,8 @@ cudaError_t launch_swept(int problem, const SweptArgs& a, cudaStream_t s) {
     if (problem == 0 && a.colB == 16) return launch_heat_col<16>(a, s);
     if (problem == 0 && a.colB == 8) return launch_heat_col<8>(a, s);
     if (problem == 0 && a.colB == 32) return launch_heat_col<32>(a, s);
+    if (problem == 0 && a.colB == 12) return launch_heat_col<12>(a, s);
+    if (problem == 0 && a.colB == 24) return launch_heat_col<24>(a, s);
     if (problem == 0) {
         const size_t per_inst = static_cast<size_t>(a.smem_doubles) * sizeof(double);
         auto go = [&](auto kern, int wpc) {

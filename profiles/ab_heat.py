@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--blocks", default="16")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--kernels", default="generic,column")
+    ap.add_argument("--problem", default="heat")
     args = ap.parse_args()
     import numpy as np
     import paper_2105_10332_b200 as sg
@@ -31,7 +32,7 @@ def main():
         ref = None
         for kern in args.kernels.split(","):
             os.environ["SG_HEAT_KERNEL"] = kern
-            cfg = sg.SolverConfig(problem="heat", nx=args.nx, block=b, steps=args.steps)
+            cfg = sg.SolverConfig(problem=args.problem, nx=args.nx, block=b, steps=args.steps)
             s = sg.Solver(cfg)
             for _ in range(2):
                 s.reset()
@@ -56,7 +57,7 @@ def main():
             else:
                 same = bool(np.array_equal(ref, r.final_field.data))
             upd = r.record.cell_updates
-            print(json.dumps({"nx": args.nx, "block": b, "kernel": kern, "steps": r.record.actual_steps,
+            print(json.dumps({"problem": args.problem, "nx": args.nx, "block": b, "kernel": kern, "steps": r.record.actual_steps,
                               "solve_s": min(t), "updates_per_s": upd / min(t),
                               "dominant_launch_ms": 1e3 * k["seconds"] / max(1, k["launches"]),
                               "dominant_launches": k["launches"],

@@ -2,7 +2,7 @@
 swept_heat_col_kernel: bitwise equal to the generic table-driven kernels and
 to the CPU oracle over many swept cycles, for every supported block size,
 with partitions (edge instances push their records into neighbours' ghost
-rings) and with the output level falling inside each phase kind."""
+rings; b = 12 / 24 leave the last lanes of each warp dead) and with the output level falling inside each phase kind."""
 import numpy as np
 import pytest
 
@@ -24,7 +24,8 @@ def _solve(sg, monkeypatch, kernel, **kw):
     return sg.run(sg.SolverConfig(problem="heat", **kw))
 
 
-@pytest.mark.parametrize("block,nx,steps", [(8, 128, 97), (16, 256, 190), (32, 512, 200)])
+@pytest.mark.parametrize("block,nx,steps", [(8, 128, 97), (12, 192, 150), (16, 256, 190), (24, 384, 160),
+                                             (32, 512, 200)])
 def test_column_matches_generic_and_oracle(sg, oracle, monkeypatch, block, nx, steps):
     _need_gpu(sg)
     col = _solve(sg, monkeypatch, "column", nx=nx, block=block, steps=steps)
@@ -34,7 +35,8 @@ def test_column_matches_generic_and_oracle(sg, oracle, monkeypatch, block, nx, s
     assert np.array_equal(col.final_field.data, _oracle_final(oracle, nx, nx, col.final_field.level))
 
 
-@pytest.mark.parametrize("block,nx,ny,px,py", [(32, 256, 256, 2, 2), (8, 128, 64, 2, 1), (16, 192, 384, 3, 2)])
+@pytest.mark.parametrize("block,nx,ny,px,py", [(32, 256, 256, 2, 2), (8, 128, 64, 2, 1), (16, 192, 384, 3, 2),
+                                               (12, 144, 96, 3, 2), (24, 192, 96, 2, 2)])
 def test_column_partitions(sg, oracle, monkeypatch, block, nx, ny, px, py):
     _need_gpu(sg)
     res = _solve(sg, monkeypatch, "column", nx=nx, ny=ny, block=block, steps=61, ranks=px * py, px=px, py=py)
