@@ -50,3 +50,17 @@ def test_column_output_level_in_every_phase(sg, oracle, monkeypatch, steps):
     _need_gpu(sg)
     res = _solve(sg, monkeypatch, "column", nx=64, block=16, steps=steps)  # forced: 16 instances
     assert np.array_equal(res.final_field.data, _oracle_final(oracle, 64, 64, res.final_field.level))
+
+
+@pytest.mark.parametrize("block", [16, 32])
+def test_full_size_swept_equals_standard(sg, block):
+    """BASELINE configs[4] grid (8192^2, one GPU), too big for the CPU oracle:
+    the swept solve (register-tile kernels, every instance, ghost-ring edges)
+    equals the standard solve bit for bit at the swept engine's final level
+    (the standard engine itself is pinned to the oracle at small sizes)."""
+    _need_gpu(sg)
+    sw = sg.run(sg.SolverConfig(problem="heat", nx=8192, block=block, steps=120, engine="swept"))
+    st = sg.run(sg.SolverConfig(problem="heat", nx=8192, block=block, steps=sw.record.actual_steps,
+                                engine="standard"))
+    assert sw.final_field.level == st.final_field.level
+    assert np.array_equal(sw.final_field.data, st.final_field.data)
