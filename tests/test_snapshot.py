@@ -35,11 +35,30 @@ def test_reader_parses_handmade_stream(sg, tmp_path):
         sg.SnapshotReader(str(p))
 
 
+HEAT_SWEPT = [c for c in GOLD["snapshots"]
+              if c["cfg"]["problem"] == "heat" and c["cfg"].get("engine", "swept") == "swept"]
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("case", GOLD["snapshots"], ids=lambda c: json.dumps(c["cfg"], sort_keys=True))
 def test_snapshot_stream_is_byte_identical_to_reference(sg, tmp_path, case):
     if sg.device_count() < 1:
         pytest.fail("no CUDA device")
+    _check_snapshot(sg, tmp_path, case)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", HEAT_SWEPT, ids=lambda c: json.dumps(c["cfg"], sort_keys=True))
+def test_register_tile_snapshot_stream_is_byte_identical(sg, tmp_path, monkeypatch, case):
+    """The same reference streams written by the register-tile heat kernels
+    (every snapshot level leaves through their stash / put_cells path)."""
+    if sg.device_count() < 1:
+        pytest.fail("no CUDA device")
+    monkeypatch.setenv("SG_HEAT_KERNEL", "column")
+    _check_snapshot(sg, tmp_path, case)
+
+
+def _check_snapshot(sg, tmp_path, case):
     path = tmp_path / "snap.bin"
     cfg = dict(case["cfg"], snapshot=str(path))
     res = sg.run(sg.SolverConfig.from_json(cfg))
