@@ -316,6 +316,21 @@ def main():
             "launches_per_step": k["launches"], "share_of_step": round(k["seconds"] * args.steps / sw_dev, 4),
             "traffic_source": nt[1] if nt else None}
     sw.close()
+    # whole-solve roofline of SURVEY.md §8d: updates/s over
+    # min(HBM / algorithmic bytes per update, FP64 non-FMA peak / flops per update)
+    fp64 = sg.measure_fp64_peak() if rank == 0 else -1.0
+    bpu = {8: 15.50, 12: 10.44, 16: 7.875, 24: 5.28, 32: 3.97}.get(BLOCK)
+    solve_roof = None
+    if bpu and fp64 > 0:
+        ceil_hbm = peaks["hbm_gbs"] * 1e9 / bpu
+        ceil_fp64 = fp64 / 9.0
+        ceil = min(ceil_hbm, ceil_fp64)
+        solve_roof = {"achieved": value / n, "unit": "cell-updates/s per GPU", "ceiling": ceil,
+                      "frac": round(value / n / ceil, 4),
+                      "bound": "hbm" if ceil_hbm <= ceil_fp64 else "fp64",
+                      "alg_bytes_per_update": bpu, "flops_per_update": 9,
+                      "fp64_nonfma_peak_flops": fp64, "fp64_peak_source": "measured (sg_measure_fp64_peak: DADD+DMUL "
+                      "chains, 8 per thread, 8 CTAs x 256 threads per SM)"}
 
     extra = {}
     if not args.no_extra:
@@ -331,7 +346,10 @@ def main():
         sb, sb_dev, sb_k, _ = timed("swept", False, block=32)
         sb_rec = sb.fetch().record
         sb.close()
-        extra["swept_b32"] = {"value": sb_rec.cell_updates * args.steps / sb_dev, "unit": "cell-updates/s",
+        b32v = sb_rec.cell_updates * args.steps / sb_dev
+        extra["swept_b32"] = {"value": b32v, "unit": "cell-updates/s",
+                              "solve_roofline_frac": round(b32v / n / min(peaks["hbm_gbs"] * 1e9 / 3.97, fp64 / 9.0), 4)
+                              if fp64 > 0 else None,
                               "actual_steps": sb_rec.actual_steps, "ms_per_step": 1e3 * sb_dev / args.steps,
                               "swept_over_standard": (sb_rec.cell_updates * args.steps / sb_dev) /
                               (st_rec.cell_updates / st_rec.actual_steps * sb_rec.actual_steps * args.steps / st_dev)}
@@ -407,7 +425,7 @@ def main():
             "e2e": {"value": e2e_value, "unit": "cell-updates/s", "h2d_bytes_per_step": nv * nx * ny * 8,
                     "d2h_bytes_per_step": nv * nx * ny * 8},
             "gpu_launches": launches,
-            "roofline": roof, "cpu_baseline": cpu, "clocks": ck,
+            "roofline": roof, "solve_roofline": solve_roof, "cpu_baseline": cpu, "clocks": ck,
             "actual_steps": rec.actual_steps, "cell_updates_per_step": updates,
             "wall_ms_per_step": 1e3 * sw_wall / args.steps,
             "multi_gpu": "one process per GPU; partition-edge records pushed by P2P stores from the phase "

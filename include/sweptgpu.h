@@ -172,6 +172,11 @@ int sg_plan_info(int problem, int block, long steps, long* stats, char* text, si
 
 /* ----------------------------------------------------- equation plugin -- */
 
+/* Measured FP64 throughput of the current device without FMA (DADD + DMUL,
+ * the solver's arithmetic), in flop/s; -1 without a device.  Diagnostic for
+ * the FP64 roofline; no reference counterpart. */
+double sg_measure_fp64_peak(void);
+
 /* Plan arithmetic, geometry.cpp:59-66 and 169-184.  Returns k / m or -1. */
 int sg_max_levels(int block, int halo);
 long sg_schedule(long requested_steps, int block, int halo, int substeps, long* flat_level);

@@ -499,6 +499,11 @@ class SnapshotReader:
         return self._frames
 
 
+def measure_fp64_peak() -> float:
+    """FP64 flop/s of cuda:0 without FMA (DADD + DMUL chains), -1 without a GPU."""
+    return float(_c.load().sg_measure_fp64_peak())
+
+
 # ------------------------------------------------------- geometry / plugin --
 def max_levels(b: int, n: int) -> int:
     """geometry.cpp:59-66; raises InvalidArgument like the reference."""

@@ -194,6 +194,8 @@ void sg_free_result(sg_result* r) {
     r->final_field = nullptr;
 }
 
+double sg_measure_fp64_peak(void) { return sg::measure_fp64_peak(); }
+
 int sg_max_levels(int block, int halo) {
     try {
         return sg::max_levels(block, halo);

@@ -1007,7 +1007,50 @@ __global__ void dist_barrier_kernel(unsigned long long* const* peer_flags, unsig
     __threadfence_system();
 }
 
+// FP64 pipe peak without FMA (the solver's arithmetic, -fmad=false): 8
+// independent DADD/DMUL chains per thread, 2 ops per chain step.
+__global__ void __launch_bounds__(256) fp64_peak_kernel(double* out, int iters, double a, double b) {
+    double x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-9 + k;
+    for (int i = 0; i < iters; ++i)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = x[k] * a + b;  // DMUL + DADD (no contraction)
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += x[k];
+    if (s == 1234.5) out[0] = s;  // keep the chains alive
+}
+
 }  // namespace
+
+double measure_fp64_peak() {
+    int dev = 0, nsm = 148;
+    if (cudaGetDevice(&dev) != cudaSuccess) return -1.0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    double* out = nullptr;
+    if (cudaMalloc(&out, sizeof(double)) != cudaSuccess) return -1.0;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int blocks = nsm * 8, iters = 4096;
+    fp64_peak_kernel<<<blocks, 256>>>(out, 64, 0.999999, 1e-7);  // warm-up
+    float best = 1e30f;
+    for (int rep = 0; rep < 5; ++rep) {
+        cudaEventRecord(e0);
+        fp64_peak_kernel<<<blocks, 256>>>(out, iters, 0.999999, 1e-7);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        best = ms < best ? ms : best;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    if (cudaGetLastError() != cudaSuccess) return -1.0;
+    return 2.0 * 8.0 * iters * blocks * 256.0 / (best * 1e-3);
+}
 
 cudaError_t launch_dist_barrier(unsigned long long* const* peer_flags, unsigned long long* my_flags, int world,
                                 int rank, unsigned long long epoch, int* err, cudaStream_t s) {

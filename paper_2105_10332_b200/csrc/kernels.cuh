@@ -91,4 +91,7 @@ struct StdArgs {
     int* err;
 };
 
+// FP64 flop/s of the current device without FMA (kernels.cu), -1 on error
+double measure_fp64_peak();
+
 }  // namespace sg

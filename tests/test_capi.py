@@ -15,7 +15,7 @@ def test_library_exports_every_declared_symbol(sg):
     from paper_2105_10332_b200 import _capi
     lib = _capi.load()
     hdr = (ROOT / "include" / "sweptgpu.h").read_text()
-    declared = set(re.findall(r"\b(sg_[a-z_]+)\s*\(", hdr))
+    declared = set(re.findall(r"\b(sg_[a-z0-9_]+)\s*\(", hdr))
     assert declared, "header parse failed"
     for name in sorted(declared):
         assert hasattr(lib, name), f"{name} declared in sweptgpu.h but not exported"
