@@ -64,3 +64,12 @@ def test_full_size_swept_equals_standard(sg, block):
                                 engine="standard"))
     assert sw.final_field.level == st.final_field.level
     assert np.array_equal(sw.final_field.data, st.final_field.data)
+
+
+@pytest.mark.parametrize("block,nx,ny", [(16, 48, 80), (32, 96, 96), (8, 24, 40), (12, 36, 60), (24, 72, 48)])
+def test_column_partial_last_cta(sg, oracle, monkeypatch, block, nx, ny):
+    """Instance counts that are not a multiple of the instances per CTA: the
+    last CTA carries dead instances that run the shuffles but write nothing."""
+    _need_gpu(sg)
+    res = _solve(sg, monkeypatch, "column", nx=nx, ny=ny, block=block, steps=40)
+    assert np.array_equal(res.final_field.data, _oracle_final(oracle, nx, ny, res.final_field.level))
