@@ -1,11 +1,14 @@
 // sm_100a kernels of the swept solver.
 //
-//  swept_heat_kernel / swept_euler_kernel: one launch = one swept phase
+//  swept_heat_col_kernel (heat, b = 8/12/16/24/32; the bench path) /
+//  swept_heat_kernel (heat on tiny grids, SG_HEAT_KERNEL=generic) /
+//  swept_euler_kernel: one launch = one swept phase
 //      (UpPyramid, YBridge, XBridge, Octahedron = OctahedronDown+OctahedronUp,
 //      DownPyramid) for every block instance of the partitions on this GPU:
 //        1. gather: imported edge cells (records of earlier phases, or the
 //           initial plane) -> shared memory (cp.async, straight to place);
-//        2. advance all levels of the phase on chip;
+//        2. advance all levels of the phase on chip (register tiles for the
+//           column kernel, shared memory for the others);
 //        3. scatter: the cells later phases read (this instance's record)
 //           -> HBM, plus the copies partition-edge instances push into the
 //           neighbouring partitions' ghost records (NVLink P2P stores when
@@ -18,6 +21,7 @@
 //      point-wise fallback for odd partition widths.
 //  substep_rects_kernel<PROB>: run_substep on rectangles (physics.cpp:551-575).
 //  dist_barrier_kernel: cross-process launch ordering (one process per GPU).
+//  fp64_peak_kernel: DADD+DMUL microbenchmark for the FP64 roofline.
 #include <cuda_runtime.h>
 
 #include <cstdlib>
