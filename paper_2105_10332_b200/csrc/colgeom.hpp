@@ -113,7 +113,7 @@ SG_HD constexpr int imp_base(int kind, int B, int r, int y) {
     for (int yy = ylo(kind, B); yy < y; ++yy) s += imp_row(kind, B, r, yy).count();
     return s;
 }
-SG_HD constexpr int exp_base(int kind, int B, int r, int y) {
+SG_HD constexpr int exp_base_rm(int kind, int B, int r, int y) {
     int s = 0;
     for (int rr = 1; rr < r; ++rr)
         for (int yy = ylo(kind, B); yy < ylo(kind, B) + B; ++yy) s += exp_row(kind, B, rr, yy).count();
@@ -121,7 +121,6 @@ SG_HD constexpr int exp_base(int kind, int B, int r, int y) {
     return s;
 }
 SG_HD constexpr int imp_total(int kind, int B) { return imp_base(kind, B, nlev(kind, B) + 1, ylo(kind, B)); }
-SG_HD constexpr int exp_total(int kind, int B) { return exp_base(kind, B, nlev(kind, B) + 1, ylo(kind, B)); }
 
 // slot of an imported cell at level r-1 (column x, row y), -1 if not an import
 SG_HD constexpr int imp_slot(int kind, int B, int r, int x, int y) {
@@ -129,11 +128,107 @@ SG_HD constexpr int imp_slot(int kind, int B, int r, int x, int y) {
     const RowSet s = imp_row(kind, B, r, y);
     return s.has(x) ? imp_base(kind, B, r, y) + s.rank(x) : -1;
 }
+// Record layout of the exports, grouped by who reads them (so that the
+// cells one consumer launch reads from a record are contiguous and whole
+// 128-byte lines serve it; with a plain level/row order the lines a launch
+// touches are shared with cells other launches read, 1.7x the read bytes):
+//   G1: the band cells (left/right columns) of the rows with a hole -- read
+//       by the horizontal neighbours,
+//   G3: the band cells of the full rows (the corners),
+//   G2: the middle cells of the full rows -- read by the vertical neighbours,
+// in the order [G1][G3][G2]; within a group by level, row, column.  A level's
+// band is [x0, x1) minus the middle [mp, mq) (the hole of its hole rows; a
+// level without hole rows has no band).
+struct ExpLev {
+    int x0, x1, mp, mq;  // R_r columns; middle columns
+    int yh0, nh;         // hole rows [yh0, yh0 + nh)
+    int ytop, ntop;      // full rows: a top run ...
+    int ybot, nbot;      // ... and a bottom run
+    int g1, g3, g2;      // first record index of the level in each group
+    SG_HD constexpr int bw() const { return (mp - x0) + (x1 - mq); }
+    SG_HD constexpr int mw() const { return mq - mp; }
+    SG_HD constexpr int nf() const { return ntop + nbot; }
+    SG_HD constexpr int count() const { return nh * bw() + nf() * (bw() + mw()); }
+    SG_HD constexpr bool band(int x) const { return x >= x0 && x < x1 && !(x >= mp && x < mq); }
+    SG_HD constexpr bool mid(int x) const { return x >= mp && x < mq; }
+    SG_HD constexpr int rank_band(int x) const { return x - x0 - (x >= mq ? mq - mp : 0); }
+    SG_HD constexpr bool hole_row(int y) const { return y >= yh0 && y < yh0 + nh; }
+    SG_HD constexpr int full_index(int y) const {  // -1: not a full row
+        return (y >= ytop && y < ytop + ntop) ? y - ytop : (y >= ybot && y < ybot + nbot) ? ntop + (y - ybot) : -1;
+    }
+    SG_HD constexpr int slot(int x, int y) const {
+        if (hole_row(y)) return band(x) ? g1 + (y - yh0) * bw() + rank_band(x) : -1;
+        const int f = full_index(y);
+        if (f < 0 || x < x0 || x >= x1) return -1;
+        return band(x) ? g3 + f * bw() + rank_band(x) : g2 + f * mw() + (x - mp);
+    }
+};
+constexpr int kMaxLevCap = 32;
+struct ExpLayout {
+    ExpLev lev[kMaxLevCap];
+    int total;
+};
+SG_HD constexpr ExpLayout exp_layout(int kind, int B) {
+    ExpLayout L{};
+    const int nl = nlev(kind, B);
+    int t1 = 0, t3 = 0, t2 = 0;
+    for (int r = 1; r <= nl; ++r) {
+        ExpLev c{};
+        const CRect q = rect(kind, B, r);
+        c.x0 = q.x0;
+        c.x1 = q.x1;
+        c.mp = q.x0;
+        c.mq = q.x1;
+        bool holes = false;
+        for (int y = ylo(kind, B); y < ylo(kind, B) + B; ++y) {
+            const RowSet s = exp_row(kind, B, r, y);
+            if (s.count() == 0) continue;
+            if (s.hq > s.hp) {  // a hole row
+                if (c.nh == 0) c.yh0 = y;
+                ++c.nh;
+                c.mp = s.hp;
+                c.mq = s.hq;
+                holes = true;
+            } else if (c.nh == 0 && c.nbot == 0 && (c.ntop == 0 || y == c.ytop + c.ntop)) {
+                if (c.ntop == 0) c.ytop = y;
+                ++c.ntop;
+            } else {
+                if (c.nbot == 0) c.ybot = y;
+                ++c.nbot;
+            }
+        }
+        if (!holes) {
+            c.mp = q.x0;
+            c.mq = q.x1;
+        }
+        c.g1 = t1;
+        t1 += c.nh * c.bw();
+        c.g3 = t3;
+        t3 += c.nf() * c.bw();
+        c.g2 = t2;
+        t2 += c.nf() * c.mw();
+        L.lev[r] = c;
+    }
+    for (int r = 1; r <= nl; ++r) {
+        L.lev[r].g3 += t1;
+        L.lev[r].g2 += t1 + t3;
+    }
+    L.total = t1 + t3 + t2;
+    return L;
+}
+// b = 32 keeps the plain level/row/column order: its records are large
+// enough that the lines each launch reads are already 90 % useful (1.11x vs
+// 1.10x grouped) and the grouped store code costs the 30-level Octahedron
+// ~50 registers (2 instead of 3 resident CTAs)
+SG_HD constexpr bool grouped_exports(int B) { return B < 32; }
+SG_HD constexpr int exp_total(int kind, int B) {
+    return grouped_exports(B) ? exp_layout(kind, B).total : exp_base_rm(kind, B, nlev(kind, B) + 1, ylo(kind, B));
+}
 // record index of an exported cell at level r, -1 if not exported
 SG_HD constexpr int exp_slot(int kind, int B, int r, int x, int y) {
-    if (y < ylo(kind, B) || y >= ylo(kind, B) + B) return -1;
     const RowSet s = exp_row(kind, B, r, y);
-    return s.has(x) ? exp_base(kind, B, r, y) + s.rank(x) : -1;
+    if (!s.has(x)) return -1;
+    return grouped_exports(B) ? exp_layout(kind, B).lev[r].slot(x, y) : exp_base_rm(kind, B, r, y) + s.rank(x);
 }
 
 // Row types of a level: the distinct RowSets among its rows, in row order
@@ -204,11 +299,12 @@ struct Run {
 };
 constexpr int kMaxRuns = 6;
 struct Tables {
-    RowSet imp[kMaxNL + 1][kMaxB], exp[kMaxNL + 1][kMaxB];
+    RowSet imp[kMaxNL + 1][kMaxB], expr[kMaxNL + 1][kMaxB];
     Run imp_runs[kMaxNL + 1][kMaxRuns], exp_runs[kMaxNL + 1][kMaxRuns];
     int imp_base[kMaxNL + 2][kMaxB], exp_base[kMaxNL + 2][kMaxB];
     int imp_type[kMaxNL + 1][kMaxB], exp_type[kMaxNL + 1][kMaxB];
     RowSet imp_tset[kMaxNL + 1][4], exp_tset[kMaxNL + 1][2];
+    ExpLayout exp;  // grouped layout (b < 32); the exp_* row tables: row-major (b = 32)
 };
 template <int NT>
 SG_HD constexpr void fill_types(const RowSet (&rows)[kMaxNL + 1][kMaxB], int nl, int B, int (&type)[kMaxNL + 1][kMaxB],
@@ -259,15 +355,16 @@ SG_HD constexpr Tables make_tables(int kind, int B) {
             t.exp_base[r][i] = se;
             if (r <= nl) {
                 t.imp[r][i] = imp_row(kind, B, r, y0 + i);
-                t.exp[r][i] = exp_row(kind, B, r, y0 + i);
+                t.expr[r][i] = exp_row(kind, B, r, y0 + i);
                 si += t.imp[r][i].count();
-                se += t.exp[r][i].count();
+                se += t.expr[r][i].count();
             }
         }
     fill_types<4>(t.imp, nl, B, t.imp_type, t.imp_tset);
-    fill_types<2>(t.exp, nl, B, t.exp_type, t.exp_tset);
+    fill_types<2>(t.expr, nl, B, t.exp_type, t.exp_tset);
     fill_runs(t.imp_type, t.imp_base, t.imp, nl, B, t.imp_runs);
-    fill_runs(t.exp_type, t.exp_base, t.exp, nl, B, t.exp_runs);
+    fill_runs(t.exp_type, t.exp_base, t.expr, nl, B, t.exp_runs);
+    t.exp = exp_layout(kind, B);
     return t;
 }
 template <int KIND, int B>

@@ -498,8 +498,73 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
                 }
             });
         }
-        // ---------------- 3. exports of level r
-        if (live) {
+        // ---------------- 3. exports of level r (grouped layout, colgeom.hpp ExpLev)
+        if constexpr (col::grouped_exports(B)) if (live) {
+            constexpr col::ExpLev E = col::Geo<KIND, B>::t.exp.lev[r];
+            if constexpr (E.count() > 0) {
+                if constexpr (MODE == col::COL) {
+                    bool pb[CPL], pm[CPL];
+                    double* gh_[CPL];
+                    double* gc[CPL];
+                    double* gm[CPL];
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) {
+                        const int c = CPL * l + q;
+                        pb[q] = E.band(c);
+                        pm[q] = E.mid(c) && c >= E.x0 && c < E.x1;
+                        const int rb = pb[q] ? E.rank_band(c) : 0;
+                        gh_[q] = dst + (E.g1 + rb - E.yh0 * E.bw());  // hole rows: + y * bw
+                        gc[q] = dst + (E.g3 + rb);                     // full rows, band: + f * bw
+                        gm[q] = dst + (E.g2 + (pm[q] ? c - E.mp : 0)); // full rows, middle: + f * mw
+                    }
+                    sfor<B>([&](auto YI) {
+                        constexpr int j = decltype(YI)::value;
+                        constexpr col::ExpLev Ej = col::Geo<KIND, B>::t.exp.lev[r];
+                        constexpr int y = YLO + j;
+                        constexpr int f = Ej.full_index(y);
+                        if constexpr (Ej.hole_row(y)) {
+#pragma unroll
+                            for (int q = 0; q < CPL; ++q) stg_if(gh_[q] + y * Ej.bw(), v[q][j], pb[q]);
+                        } else if constexpr (f >= 0) {
+                            if constexpr (Ej.bw() > 0) {
+#pragma unroll
+                                for (int q = 0; q < CPL; ++q) stg_if(gc[q] + f * Ej.bw(), v[q][j], pb[q]);
+                            }
+#pragma unroll
+                            for (int q = 0; q < CPL; ++q) stg_if(gm[q] + f * Ej.mw(), v[q][j], pm[q]);
+                        }
+                    });
+                } else {
+                    bool pbr[CPL], pmr[CPL];
+                    double* gb[CPL];
+                    double* gm[CPL];
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) {
+                        const int y = YLO + CPL * l + q;  // the lane's window row
+                        const bool hole = E.hole_row(y);
+                        const int f = E.full_index(y);
+                        pbr[q] = hole || f >= 0;
+                        pmr[q] = f >= 0;
+                        gb[q] = dst + (hole ? E.g1 + (y - E.yh0) * E.bw() : E.g3 + (f >= 0 ? f : 0) * E.bw());
+                        gm[q] = dst + (E.g2 + (f >= 0 ? f : 0) * E.mw() - E.mp);
+                    }
+                    sfor<B>([&](auto XI) {
+                        constexpr int x = decltype(XI)::value;
+                        constexpr col::ExpLev Ex = col::Geo<KIND, B>::t.exp.lev[r];
+                        if constexpr (Ex.band(x)) {
+                            constexpr int rk = Ex.rank_band(x);
+#pragma unroll
+                            for (int q = 0; q < CPL; ++q) stg_if(gb[q] + rk, v[q][x], pbr[q]);
+                        } else if constexpr (Ex.mid(x) && x >= Ex.x0 && x < Ex.x1) {
+#pragma unroll
+                            for (int q = 0; q < CPL; ++q) stg_if(gm[q] + x, v[q][x], pmr[q]);
+                        }
+                    });
+                }
+            }
+        }
+        // b = 32: row-major record (colgeom.hpp grouped_exports)
+        if constexpr (!col::grouped_exports(B)) if (live) {
             if constexpr (MODE == col::COL) {
                 bool ep[CPL][2];
                 double* eg[CPL][2];

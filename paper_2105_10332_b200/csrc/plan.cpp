@@ -439,18 +439,24 @@ SweptPlan compile_swept_plan(int b, const Equation& eq, long m, long final_level
             K.exp_off.clear();
             K.exp_vstride.clear();
             K.exp_pairs.clear();
+            std::vector<std::array<int, 3>> by_slot(static_cast<std::size_t>(col::exp_total(kd, b)), {-1, 0, 0});
             for (int r = 1; r <= K.nlev; ++r)
                 for (int y = col::ylo(kd, b); y < col::ylo(kd, b) + b; ++y)
                     for (int x = 0; x < b; ++x)
                         if (col::exp_row(kd, b, r, y).has(x)) {
-                            if (col::exp_slot(kd, b, r, x, y) != static_cast<int>(K.exp_cells.size()))
-                                fail(SG_ELOGIC, "plan: column export order");
+                            const int sl = col::exp_slot(kd, b, r, x, y);
+                            if (sl < 0 || sl >= static_cast<int>(by_slot.size()) || by_slot[sl][0] >= 0)
+                                fail(SG_ELOGIC, "plan: column export layout is not a bijection");
+                            by_slot[sl] = {r, x, y};
                             formula.insert({r, x, y});
-                            K.exp_cells.push_back({r, x, y});
-                            K.exp_off.push_back(0);
-                            K.exp_vstride.push_back(0);
-                            K.exp_pairs.push_back({0, static_cast<int>(K.exp_pairs.size())});
                         }
+            for (const auto& c : by_slot) {
+                if (c[0] < 0) fail(SG_ELOGIC, "plan: column export layout has a gap");
+                K.exp_cells.push_back(c);
+                K.exp_off.push_back(0);
+                K.exp_vstride.push_back(0);
+                K.exp_pairs.push_back({0, static_cast<int>(K.exp_pairs.size())});
+            }
             if (static_cast<int>(K.exp_cells.size()) != col::exp_total(kd, b))
                 fail(SG_ELOGIC, "plan: column export count");
             for (auto& kv : exp_mask[kd])
