@@ -184,7 +184,7 @@ def workload_config(n, nx, ny):
 
 
 def main():
-    global PER_GPU, REQ_STEPS
+    global PER_GPU, REQ_STEPS, BLOCK
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -195,8 +195,11 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--no-extra", action="store_true", help="skip the standard / Euler side measurements")
     ap.add_argument("--ref-sample-steps", type=int, default=21)
+    ap.add_argument("--block", type=int, default=BLOCK,
+                    help="swept block size (default 16, the reference weak-scaling block; 32 is the fastest here)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    BLOCK = args.block
 
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
