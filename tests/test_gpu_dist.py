@@ -73,3 +73,33 @@ def test_two_process_partitions_bitwise(sg, oracle, monkeypatch, engine, kernel,
     want = oracle.standard_solve(P, init, level, params)
     assert np.array_equal(data, want)
     assert msgs > 0
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("engine,kernel,problem", [("swept", "column", "heat"), ("swept", "generic", "heat"),
+                                                   ("standard", "generic", "heat"), ("swept", "generic", "euler")])
+def test_four_process_2x2_partitions_bitwise(sg, oracle, monkeypatch, engine, kernel, problem):
+    """2 x 2 partitions, one process each: partition-corner instances push
+    their records to the diagonal neighbour's ghost ring too (three peers)."""
+    if sg.device_count() < 1:
+        pytest.fail("no CUDA device")
+    monkeypatch.setenv("SG_HEAT_KERNEL", kernel)
+    import torch.multiprocessing as mp
+    nx = 64
+    cfgd = dict(problem=problem, nx=nx, block=16 if problem == "heat" else 8, steps=12, engine=engine,
+                ranks=4, px=2, py=2)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 4, port, cfgd, q)) for r in range(4)]
+    for p in procs:
+        p.start()
+    status, data, level, msgs = q.get(timeout=500)
+    for p in procs:
+        p.join(timeout=120)
+    assert status == "ok", data
+    P = oracle.HEAT if problem == "heat" else oracle.EULER
+    init, params = oracle.params(P, nx)
+    want = oracle.standard_solve(P, init, level, params)
+    assert np.array_equal(data, want)
+    assert msgs > 0
