@@ -121,7 +121,8 @@ Solver::Solver(const sg_config& cfg, int rank, int world) : cfg_(cfg), rank_(ran
         total_levels_ = flat;
         final_level_ = actual_steps_ * eq.substeps;  // engine.cpp:518
         plan_ = compile_swept_plan(cfg_.block, eq, m, final_level_,
-                                   static_cast<long>(setup_.nx / cfg_.block) * (setup_.ny / cfg_.block));
+                                   static_cast<long>(setup_.nx / cfg_.block) * (setup_.ny / cfg_.block),
+                                   static_cast<long>(pw_ / cfg_.block + 2) * (ph_ / cfg_.block + 2));
         for (const Launch& l : plan_.launches)
             cell_updates_ += static_cast<long long>(plan_.updates_per_kind[l.kind]) *
                              (setup_.nx / cfg_.block) * (setup_.ny / cfg_.block);

@@ -128,8 +128,11 @@ void spread_banks(std::vector<T>& v, std::size_t begin, std::size_t end, Key key
 // b in {8, 16, 32} use the register-tile kernels (colgeom.hpp) unless
 // SG_HEAT_KERNEL=generic is set, or the grid is so small (< 2048 instances)
 // that the per-instance latency of the generic kernels wins (SG_HEAT_KERNEL=
-// column forces them).
-SweptPlan compile_swept_plan(int b, const Equation& eq, long m, long final_level, long instances = 0);
+// column forces them), or a partition so large that the record ring of one
+// partition (7 slots) would exceed the kernels' 32-bit gather offsets
+// (partition_instances = (pw/b + 2) * (ph/b + 2), ghost ring included).
+SweptPlan compile_swept_plan(int b, const Equation& eq, long m, long final_level, long instances = 0,
+                             long partition_instances = 0);
 
 std::string describe_plan(const SweptPlan& p);
 

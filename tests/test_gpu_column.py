@@ -73,3 +73,15 @@ def test_column_partial_last_cta(sg, oracle, monkeypatch, block, nx, ny):
     _need_gpu(sg)
     res = _solve(sg, monkeypatch, "column", nx=nx, ny=ny, block=block, steps=40)
     assert np.array_equal(res.final_field.data, _oracle_final(oracle, nx, ny, res.final_field.level))
+
+
+def test_huge_partition_falls_back_to_generic_kernels(sg):
+    """16384^2 on one GPU: 7 record slots of (1026^2 instances x 392 cells)
+    exceed the register-tile kernels' 32-bit gather offsets, so the plan
+    picks the generic kernels (64-bit segment bases); still equal to the
+    standard solve."""
+    _need_gpu(sg)
+    sw = sg.run(sg.SolverConfig(problem="heat", nx=16384, block=16, steps=20, engine="swept"))
+    st = sg.run(sg.SolverConfig(problem="heat", nx=16384, block=16, steps=sw.record.actual_steps,
+                                engine="standard"))
+    assert np.array_equal(sw.final_field.data, st.final_field.data)
