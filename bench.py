@@ -310,7 +310,7 @@ def main():
     achieved = per_launch_bytes / per_launch_s / 1e9
     tag = workload_config(n, nx, ny)["workload"]
     nt = ncu_traffic(tag)
-    roof = {"kernel": "swept_heat_col_kernel<16, Octahedron> (register-tile Octahedron launches)", "bound": "hbm",
+    roof = {"kernel": f"swept_heat_col_kernel<{BLOCK}, Octahedron> (register-tile Octahedron launches)", "bound": "hbm",
             "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": nt[0] if nt else None,
             "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else
