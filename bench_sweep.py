@@ -29,6 +29,8 @@ def main():
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() \
         else {"hbm_gbs": 6650.0}
 
+    fp64 = sg.measure_fp64_peak()
+
     def timed(cfg, profile=False):
         s = sg.Solver(cfg)  # timed runs replay the solve's CUDA graph
         for _ in range(2):
@@ -71,6 +73,11 @@ def main():
                     gbs = ks["alg_bytes"] / ks["seconds"] / 1e9
                     line.update(oct_alg_GBps=round(gbs, 1), oct_roofline_frac=round(gbs / peaks["hbm_gbs"], 4),
                                 oct_share=round(ks["seconds"] / ts, 3))
+                    # SURVEY.md §8d whole-solve roofline: min(HBM / B_alg, FP64 / 9 flops)
+                    bpu = {8: 15.50, 12: 10.44, 16: 7.875, 24: 5.28, 32: 3.97}.get(b)
+                    if bpu and fp64 > 0:
+                        ceil = min(peaks["hbm_gbs"] * 1e9 / bpu, fp64 / 9.0)
+                        line.update(solve_roofline_frac=round(rs.record.cell_updates / ts / ceil, 4))
             except Exception as e:  # noqa: BLE001
                 line["error"] = str(e)
             print(json.dumps(line), flush=True)
