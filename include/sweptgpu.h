@@ -24,6 +24,7 @@
 #define SWEPTGPU_H
 
 #include <stddef.h>
+#include <stdint.h>
 
 #ifdef __cplusplus
 extern "C" {
@@ -190,6 +191,11 @@ long sg_schedule(long requested_steps, int block, int halo, int substeps, long* 
 int sg_substep(int problem, int stage, const double* d_read1, const double* d_read2,
                double* d_out, int nvars, int nx, int ny, const int* rects, int nrects,
                const double* params, void* stream, char* err, size_t errlen);
+
+/* FNV-1a-64 of a host buffer: the final-field fingerprint of the reference's
+ * parity probes.  Lets callers compare a solve with a
+ * reference run byte for byte without moving the field. */
+uint64_t sg_fnv1a64(const void* data, size_t bytes);
 
 /* Library version / build info string (static storage). */
 const char* sg_version(void);

@@ -8,10 +8,10 @@ Public API mirrors the reference (see api.py for the file:line mapping):
 """
 from .api import (CudaError, DistSolver, FieldState, InvalidArgument, LinkModel, LogicError, NonPhysicalState, PoolSpec,
                   RunRecord, RunResult, SnapshotFrame, SnapshotIOError, SnapshotReader, Solver, SolverConfig, SweptError, TransportError,
-                  build_schedule, device_count, max_levels, measure_fp64_peak, plan_info, run, run_distributed, substep, version)
+                  build_schedule, device_count, fnv1a64, max_levels, measure_fp64_peak, plan_info, run, run_distributed, substep, version)
 
 __all__ = [
     "CudaError", "DistSolver", "FieldState", "InvalidArgument", "LinkModel", "LogicError", "NonPhysicalState", "PoolSpec",
     "RunRecord", "RunResult", "SnapshotFrame", "SnapshotIOError", "SnapshotReader", "Solver", "SolverConfig", "SweptError", "TransportError",
-    "build_schedule", "device_count", "max_levels", "measure_fp64_peak", "plan_info", "run", "run_distributed", "substep", "version",
+    "build_schedule", "device_count", "fnv1a64", "max_levels", "measure_fp64_peak", "plan_info", "run", "run_distributed", "substep", "version",
 ]

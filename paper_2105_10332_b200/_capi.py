@@ -52,7 +52,7 @@ EXPORTS = (
     "sg_solver_reset", "sg_solver_solve", "sg_solver_fetch", "sg_solver_kernel_stats",
     "sg_solver_upload", "sg_solver_download", "sg_solver_initial", "sg_solver_set_profile", "sg_solver_destroy", "sg_plan_info", "sg_max_levels", "sg_schedule",
     "sg_measure_fp64_peak",
-    "sg_substep", "sg_version", "sg_device_count", "sg_dist_create", "sg_dist_blob", "sg_dist_connect",
+    "sg_substep", "sg_fnv1a64", "sg_version", "sg_device_count", "sg_dist_create", "sg_dist_blob", "sg_dist_connect",
 )
 
 _lib = None
@@ -101,6 +101,8 @@ def load() -> C.CDLL:
     L.sg_dist_blob.argtypes = [sp, C.c_void_p, C.c_long, C.c_char_p, C.c_size_t]
     L.sg_dist_blob.restype = C.c_long
     L.sg_dist_connect.argtypes = [sp, C.c_void_p, C.c_long, C.c_char_p, C.c_size_t]
+    L.sg_fnv1a64.argtypes = [C.c_void_p, C.c_size_t]
+    L.sg_fnv1a64.restype = C.c_uint64
     L.sg_version.argtypes = []
     L.sg_version.restype = C.c_char_p
     L.sg_device_count.argtypes = []

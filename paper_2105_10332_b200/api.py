@@ -308,6 +308,42 @@ def run(cfg: SolverConfig) -> RunResult:
         L.sg_free_result(C.byref(res))
 
 
+def _host_f64_ptr(host, shape, what: str) -> int:
+    """Address of a host float64 buffer holding exactly prod(shape) elements
+    in C order (numpy array or CPU torch tensor); InvalidArgument otherwise
+    -- the C side reads or writes that many doubles through the pointer."""
+    n = int(np.prod(shape))
+    if hasattr(host, "data_ptr"):  # torch.Tensor
+        import torch
+        if host.device.type != "cpu":
+            raise InvalidArgument(f"{what}: host buffer expected, got a {host.device} tensor")
+        if host.dtype != torch.float64:
+            raise InvalidArgument(f"{what}: float64 buffer expected, got {host.dtype}")
+        if not host.is_contiguous():
+            raise InvalidArgument(f"{what}: buffer must be contiguous")
+        if host.numel() != n:
+            raise InvalidArgument(f"{what}: buffer holds {host.numel()} values, expected {n} {tuple(shape)}")
+        return host.data_ptr()
+    if isinstance(host, np.ndarray):
+        if host.dtype != np.float64:
+            raise InvalidArgument(f"{what}: float64 buffer expected, got {host.dtype}")
+        if not host.flags.c_contiguous:
+            raise InvalidArgument(f"{what}: buffer must be C-contiguous")
+        if host.size != n:
+            raise InvalidArgument(f"{what}: buffer holds {host.size} values, expected {n} {tuple(shape)}")
+        if not host.flags.writeable and what != "upload":
+            raise InvalidArgument(f"{what}: buffer is read-only")
+        return host.ctypes.data
+    raise InvalidArgument(f"{what}: numpy array or CPU torch tensor expected, got {type(host).__name__}")
+
+
+def fnv1a64(data) -> str:
+    """FNV-1a-64 of a float64 field's bytes (hex), the fingerprint of the
+    reference's parity probes, computed by the library."""
+    a = np.ascontiguousarray(data)
+    return f"{_c.load().sg_fnv1a64(C.c_void_p(a.ctypes.data), a.nbytes):016x}"
+
+
 class Solver:
     """Resident solver (sg_solver_*): create once, then reset/solve/fetch.
     Used by bench.py to time the solve with inputs already in HBM."""
@@ -323,6 +359,7 @@ class Solver:
             rank, world = _dist
             _check(self._L.sg_dist_create(C.byref(self._cfg), rank, world, C.byref(h), err, len(err)), err)
         self._h = h
+        self._dist = _dist
         if profile:  # True: the dominant kernel; an int k >= 2: swept phase kind k - 2
             self._L.sg_solver_set_profile(self._h, int(profile))
 
@@ -346,24 +383,36 @@ class Solver:
         finally:
             self._L.sg_free_result(C.byref(res))
 
+    def _piece_shape(self):
+        """(nvars, rows, cols) of the host arrays upload/download/initial take:
+        the global field, or this rank's partition piece in a distributed run."""
+        c = self._cfg
+        nv = 1 if c.problem == _c.SG_HEAT else 4
+        ny = c.ny if c.ny > 0 else c.nx
+        if getattr(self, "_dist", None) is None:
+            return nv, ny, c.nx
+        px = c.px if c.px > 0 else (c.ranks if c.py <= 0 else 1)
+        py = c.py if c.py > 0 else 1
+        return nv, ny // py, c.nx // px
+
+    def _host_ptr(self, host, what: str) -> C.c_void_p:
+        return C.c_void_p(_host_f64_ptr(host, self._piece_shape(), what))
+
     def upload(self, host) -> None:
         """Replace level 0 from a host array [var][ny][nx] float64 (numpy, or a
         pinned torch CPU tensor): the e2e input path."""
         err = _c.errbuf()
-        p = host.data_ptr() if hasattr(host, "data_ptr") else host.ctypes.data
-        _check(self._L.sg_solver_upload(self._h, C.c_void_p(p), err, len(err)), err)
+        _check(self._L.sg_solver_upload(self._h, self._host_ptr(host, "upload"), err, len(err)), err)
 
     def download(self, host) -> None:
         """Final field into a host array [var][ny][nx] float64."""
         err = _c.errbuf()
-        p = host.data_ptr() if hasattr(host, "data_ptr") else host.ctypes.data
-        _check(self._L.sg_solver_download(self._h, C.c_void_p(p), err, len(err)), err)
+        _check(self._L.sg_solver_download(self._h, self._host_ptr(host, "download"), err, len(err)), err)
 
     def initial(self, host) -> None:
         """The initial condition make_setup computed (engine.cpp:27-70) into a host array."""
         err = _c.errbuf()
-        p = host.data_ptr() if hasattr(host, "data_ptr") else host.ctypes.data
-        _check(self._L.sg_solver_initial(self._h, C.c_void_p(p), err, len(err)), err)
+        _check(self._L.sg_solver_initial(self._h, self._host_ptr(host, "initial"), err, len(err)), err)
 
     def kernel_stats(self) -> dict:
         s, n, b, u = C.c_double(), C.c_long(), C.c_double(), C.c_double()
@@ -546,8 +595,20 @@ def substep(problem: str, stage: int, read1, read2, out, rects, params, stream=N
     p = np.ascontiguousarray(np.asarray(params, dtype=np.float64))
     err = _c.errbuf()
 
+    if nvars != (1 if problem == "heat" else 4):
+        raise InvalidArgument(f"substep: {problem} needs {1 if problem == 'heat' else 4} variables, got {nvars}")
+
     def ptr(t):
-        return C.c_void_p(t.data_ptr() if hasattr(t, "data_ptr") else int(t))
+        if hasattr(t, "data_ptr"):  # torch tensor: a device buffer of read1's shape
+            import torch
+            if not t.is_cuda:
+                raise InvalidArgument("substep: device (CUDA) tensors expected")
+            if t.dtype != torch.float64 or not t.is_contiguous():
+                raise InvalidArgument("substep: contiguous float64 tensors expected")
+            if tuple(t.shape) != (nvars, ny, nx):
+                raise InvalidArgument(f"substep: shape {tuple(t.shape)} != read1's {(nvars, ny, nx)}")
+            return C.c_void_p(t.data_ptr())
+        return C.c_void_p(int(t))  # a raw device pointer: the caller vouches for it
 
     s = C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else (stream or 0))
     rc = L.sg_substep(PROBLEMS[problem], stage, ptr(read1), ptr(read2), ptr(out), nvars, nx, ny,

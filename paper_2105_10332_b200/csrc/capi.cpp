@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <cstdint>
 #include <cstdio>
 #include <cstring>
 #include <vector>
@@ -239,15 +240,22 @@ int sg_substep(int problem, int stage, const double* d_read1, const double* d_re
             c[3] = 0.0;
         }
         auto s = static_cast<cudaStream_t>(stream);
-        int* d_rects = nullptr;
-        long* d_prefix = nullptr;
-        int* d_err = nullptr;
         auto ck = [](cudaError_t e) {
             if (e != cudaSuccess) sg::fail(SG_ECUDA, cudaGetErrorString(e));
         };
-        ck(cudaMalloc(&d_rects, sizeof(int) * 4 * std::max(nrects, 1)));
-        ck(cudaMalloc(&d_prefix, sizeof(long) * (nrects + 1)));
-        ck(cudaMalloc(&d_err, sizeof(int)));
+        // scratch freed on every path (a failing check throws through guard())
+        struct DevBuf {
+            void* p = nullptr;
+            ~DevBuf() {
+                if (p) cudaFree(p);
+            }
+        } rb, pb, eb;
+        ck(cudaMalloc(&rb.p, sizeof(int) * 4 * std::max(nrects, 1)));
+        ck(cudaMalloc(&pb.p, sizeof(long) * (nrects + 1)));
+        ck(cudaMalloc(&eb.p, sizeof(int)));
+        int* d_rects = static_cast<int*>(rb.p);
+        long* d_prefix = static_cast<long*>(pb.p);
+        int* d_err = static_cast<int*>(eb.p);
         ck(cudaMemsetAsync(d_err, 0, sizeof(int), s));
         if (nrects) ck(cudaMemcpyAsync(d_rects, rects, sizeof(int) * 4 * nrects, cudaMemcpyHostToDevice, s));
         ck(cudaMemcpyAsync(d_prefix, prefix.data(), sizeof(long) * (nrects + 1), cudaMemcpyHostToDevice, s));
@@ -256,11 +264,18 @@ int sg_substep(int problem, int stage, const double* d_read1, const double* d_re
         int e = 0;
         ck(cudaMemcpyAsync(&e, d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
         ck(cudaStreamSynchronize(s));
-        cudaFree(d_rects);
-        cudaFree(d_prefix);
-        cudaFree(d_err);
         if (e) sg::fail(SG_ENONPHYS, "non-physical state: rho <= 0 or p <= 0");
     });
+}
+
+uint64_t sg_fnv1a64(const void* data, size_t bytes) {
+    std::uint64_t h = 1469598103934665603ull;
+    const unsigned char* p = static_cast<const unsigned char*>(data);
+    for (size_t i = 0; i < bytes; ++i) {
+        h ^= p[i];
+        h *= 1099511628211ull;
+    }
+    return h;
 }
 
 const char* sg_version(void) {

@@ -63,35 +63,51 @@ Solver::Solver(const sg_config& cfg, int rank, int world) : cfg_(cfg), rank_(ran
     int ndev = 0;
     ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
     if (ndev < 1) fail(SG_ECUDA, "no CUDA device visible (the GPU solver has no CPU fallback)");
-    int use = cfg_.devices > 0 ? std::min(cfg_.devices, ndev) : ndev;
+    // SG_DEVICE_ALIAS=1 (tests only): every logical device is the current
+    // physical one, so the one-process multi-device path (per-device streams,
+    // cross-device event waits) runs on a single-GPU box
+    const bool alias = [] {
+        const char* v = std::getenv("SG_DEVICE_ALIAS");
+        return v && v[0] == '1';
+    }();
+    int use = cfg_.devices > 0 ? (alias ? cfg_.devices : std::min(cfg_.devices, ndev)) : ndev;
     use = std::min(use, nparts_);
     int dev0 = 0;
+    ck(cudaGetDevice(&dev0), "cudaGetDevice");
+    if (!dist() && !alias) dev0 = 0;  // one process, many GPUs: devices 0 .. use-1
     if (dist()) {  // one process per GPU: this rank owns partition `rank` on its current device
         if (world_ != nparts_) fail(SG_EINVAL, "distributed run: world size must equal px*py");
         if (rank_ < 0 || rank_ >= world_) fail(SG_EINVAL, "distributed run: bad rank");
-        ck(cudaGetDevice(&dev0), "cudaGetDevice");
         use = 1;
     }
     devs_.resize(use);
     for (int d = 0; d < use; ++d) {
-        devs_[d].dev = dev0 + d;
-        ck(cudaSetDevice(d), "cudaSetDevice");
+        const int phys = alias ? dev0 : dev0 + d;
+        devs_[d].dev = phys;
+        ck(cudaSetDevice(phys), "cudaSetDevice");
         ck(cudaStreamCreateWithFlags(&devs_[d].stream, cudaStreamNonBlocking), "stream");
+        {  // every launch of device d goes to a stream of device d
+            int sdev = -1;
+            ck(cudaStreamGetDevice(devs_[d].stream, &sdev), "cudaStreamGetDevice");
+            if (sdev != phys) fail(SG_ELOGIC, "stream created on the wrong device");
+        }
         ck(cudaEventCreate(&devs_[d].ev_start), "event");
         ck(cudaEventCreate(&devs_[d].ev_stop), "event");
         ck(cudaEventCreateWithFlags(&devs_[d].ev_sync, cudaEventDisableTiming), "event");
         devs_[d].d_err = dev_alloc<int>(devs_[d], 1);
-        for (int e = 0; e < use; ++e)
-            if (e != d) {
+        for (int e = 0; e < use; ++e) {
+            const int pe = alias ? dev0 : dev0 + e;
+            if (pe != phys) {
                 int can = 0;
-                cudaDeviceCanAccessPeer(&can, dev0 + d, dev0 + e);
+                cudaDeviceCanAccessPeer(&can, phys, pe);
                 if (can) {
-                    cudaError_t r = cudaDeviceEnablePeerAccess(dev0 + e, 0);
+                    cudaError_t r = cudaDeviceEnablePeerAccess(pe, 0);
                     if (r != cudaSuccess && r != cudaErrorPeerAccessAlreadyEnabled)
                         ck(r, "cudaDeviceEnablePeerAccess");
                     cudaGetLastError();
                 }
             }
+        }
     }
     parts_.resize(nparts_);
     for (int p = 0; p < nparts_; ++p) {

@@ -11,13 +11,12 @@ sys.path.insert(0, str(Path(__file__).resolve().parent))
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); run with -m gpu")
-    # a fresh checkout has no built library (it is not in git): build it once
-    # (nvcc cross-compiles sm_100a without a GPU) instead of failing every test
-    lib = ROOT / "paper_2105_10332_b200" / "libsweptgpu.so"
-    if not lib.exists():
-        import subprocess
-        subprocess.run(["make", "-C", str(ROOT / "paper_2105_10332_b200" / "csrc"), "-j8"], check=True,
-                       capture_output=True)
+    # always (re)build the library: make's dependency tracking makes this a
+    # no-op when it is current, and a stale .so must never be tested against
+    # newer sources (nvcc cross-compiles sm_100a without a GPU)
+    import subprocess
+    subprocess.run(["make", "-C", str(ROOT / "paper_2105_10332_b200" / "csrc"), "-j8"], check=True,
+                   capture_output=True)
 
 
 @pytest.fixture(scope="session")

@@ -91,3 +91,28 @@ def test_run_record_json_keys(sg):
                     "total_levels", "octahedra", "communicates", "dt", "setup_seconds", "wall_seconds",
                     "modeled_seconds", "messages", "bytes", "cell_updates", "snapshot_frames", "per_rank"]
     assert len(rec.to_json()["per_rank"]) == 2
+
+
+def test_host_buffer_validation():
+    """Solver.upload/download/initial hand a raw pointer to the C side, which
+    reads or writes nvars*ny*nx doubles: anything else is refused up front."""
+    import numpy as np
+    import torch
+    from paper_2105_10332_b200 import InvalidArgument
+    from paper_2105_10332_b200.api import _host_f64_ptr
+    shape = (1, 8, 16)
+    ok = np.zeros(shape)
+    assert _host_f64_ptr(ok, shape, "upload") == ok.ctypes.data
+    assert _host_f64_ptr(torch.zeros(shape, dtype=torch.float64), shape, "download") > 0
+    bad = [np.zeros(shape, dtype=np.float32), np.zeros((1, 8, 32))[:, :, ::2], np.zeros((1, 8, 15)),
+           torch.zeros(shape, dtype=torch.float32), torch.zeros((1, 16, 8), dtype=torch.float64).transpose(1, 2),
+           [0.0] * 128]
+    for b in bad:
+        with pytest.raises(InvalidArgument):
+            _host_f64_ptr(b, shape, "upload")
+
+
+def test_fnv1a64_matches_reference_convention(sg, oracle):
+    import numpy as np
+    a = np.arange(1000, dtype=np.float64) * 0.37
+    assert sg.fnv1a64(a) == oracle.fnv1a(a)

@@ -103,3 +103,67 @@ def test_four_process_2x2_partitions_bitwise(sg, oracle, monkeypatch, engine, ke
     want = oracle.standard_solve(P, init, level, params)
     assert np.array_equal(data, want)
     assert msgs > 0
+
+
+@pytest.mark.parametrize("engine", ["swept", "standard"])
+@pytest.mark.parametrize("problem,px,py,devices", [("heat", 2, 1, 2), ("heat", 2, 2, 4), ("euler", 2, 2, 2)])
+def test_one_process_multi_device_path(sg, oracle, monkeypatch, engine, problem, px, py, devices):
+    """One process driving several devices (partitions spread over `devices`
+    CUDA devices: per-device streams, cross-device event waits before every
+    dependent launch, run_ranks of engine.cpp:427-457).  SG_DEVICE_ALIAS=1
+    maps every logical device onto the one GPU of the test box so the path
+    runs here; on a multi-GPU box it is the same code with distinct devices."""
+    if sg.device_count() < 1:
+        pytest.fail("no CUDA device")
+    monkeypatch.setenv("SG_DEVICE_ALIAS", "1")
+    nx = 128 if problem == "heat" else 64
+    block = 16 if problem == "heat" else 8
+    res = sg.run(sg.SolverConfig(problem=problem, nx=nx, block=block, steps=12, engine=engine, ranks=px * py,
+                                 px=px, py=py, devices=devices))
+    P = oracle.HEAT if problem == "heat" else oracle.EULER
+    init, params = oracle.params(P, nx)
+    want = oracle.standard_solve(P, init, res.final_field.level, params)
+    assert np.array_equal(res.final_field.data, want)
+
+
+def _bench(args, env_extra, nproc=None):
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, **env_extra)
+    if nproc:
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+               "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py"] + args
+    else:
+        cmd = [sys.executable, "bench.py"] + args
+    p = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=800, env=env)
+    assert p.returncode == 0, (p.stdout[-2000:], p.stderr[-3000:])
+    lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, p.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("n", [2, 4])
+def test_bench_torchrun_n_ranks(sg, n):
+    """bench.py under torchrun with N ranks (the driver's N>1 launch), all
+    ranks on the one GPU of the test box (SG_BENCH_SAME_DEVICE=1, gloo): the
+    JSON line is produced by rank 0 and the assembled global field equals a
+    1-process solve of the same global grid bit for bit."""
+    if sg.device_count() < 1:
+        pytest.fail("no CUDA device")
+    per = 1024
+    args = ["--gpus", str(n), "--per-gpu", str(per), "--req-steps", "100", "--steps", "2", "--warmup", "3",
+            "--no-extra", "--no-cpu", "--hash"]
+    d = _bench(args, {"SG_BENCH_SAME_DEVICE": "1", "SG_BENCH_BACKEND": "gloo"}, nproc=n)
+    px, py = {2: (2, 1), 4: (2, 2)}[n]
+    assert d["n_gpus"] == n and d["config"]["partition"] == f"{px}x{py}"
+    assert d["config"]["nx"] == per * px and d["config"]["ny"] == per * py
+    assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
+    with sg.Solver(sg.SolverConfig(problem="heat", nx=per * px, ny=per * py, block=16, steps=100)) as s:
+        s.reset()
+        s.solve()
+        want = sg.fnv1a64(s.fetch().final_field.data)
+    assert d["final_fnv1a64"] == want
