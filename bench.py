@@ -295,6 +295,7 @@ def main():
         prof_dev += sp.solve()
         sw_k.append(sp.kernel_stats())
     prof_steps = len(sw_k)
+    sync()  # no rank frees buffers a peer may still be pushing into
     sp.close()
 
     # ---- e2e: pinned host piece in -> solve -> host piece out, every step --

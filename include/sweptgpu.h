@@ -13,7 +13,7 @@
  *
  * Errors mirror the reference's exception types as return codes:
  *   SG_EINVAL    std::invalid_argument   (config.cpp:31-62, geometry.cpp:43-66)
- *   SG_ENONPHYS  NonPhysicalState        (physics.hpp:18-20, physics.cpp:258-267)
+ *   SG_ENONPHYS  NonPhysicalState        (physics.hpp:18-20, physics.cpp:52-61)
  *   SG_ETRANSPORT TransportError         (transport.hpp:62-64)
  *   SG_EIO       std::runtime_error I/O  (snapshot.cpp:59-112, config.cpp:129)
  *   SG_ELOGIC    std::logic_error        (engine.cpp:295,565)
@@ -101,6 +101,14 @@ typedef struct sg_result {
     long snapshot_frames;
     long kernel_launches;  /* our kernels launched by the solve */
     double* final_field;   /* library-owned [var][y][x] fp64; sg_free_result */
+    /* per-partition ledger (the reference's per-rank CostLedger,
+     * transport.hpp:35-60, RunRecord::to_json per_rank, engine.cpp:482-489):
+     * messages / bytes each partition pushed into other partitions (P2P
+     * stores over NVLink between GPUs), exact counts of the launch plan.
+     * Library-owned arrays of nparts entries, freed by sg_free_result. */
+    int nparts;
+    long* part_messages;
+    long long* part_bytes;
 } sg_result;
 
 /* ---------------------------------------------------------------- solver -- */
@@ -183,7 +191,7 @@ int sg_max_levels(int block, int halo);
 long sg_schedule(long requested_steps, int block, int halo, int substeps, long* flat_level);
 
 /* One sub-step over rectangles on DEVICE buffers, the GPU replacement of
- * run_substep_serial/omp (physics.hpp:110-134, physics.cpp:551-575):
+ * run_substep_serial/omp (physics.hpp:110-134, physics.cpp:345-369):
  * layout [var][y][x] fp64, y wraps, x must stay in range (GridView contract,
  * field.hpp:12-24).  rects: nrects x {x0,x1,y0,y1} (host array).
  * params: heat {alpha,dx,dy,dt} | euler {gamma,dx,dy,dt}.  `stream` is a

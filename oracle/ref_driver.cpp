@@ -5,8 +5,8 @@
 //   run(const SolverConfig&) -> RunResult          proj/include/sweptgrid/engine.hpp:61
 //   make_setup(const SolverConfig&)                proj/src/engine.cpp:27-70
 //   build_schedule / build_schedule_cycles         proj/src/geometry.cpp:122-184
-//   run_substep_serial / run_substep_omp           proj/src/physics.cpp:551-575
-//   pressure / minmod_reconstruct / interface_flux proj/src/physics.cpp:258-313
+//   run_substep_serial / run_substep_omp           proj/src/physics.cpp:345-369
+//   pressure / minmod_reconstruct / interface_flux proj/src/physics.cpp:52-107
 // No reference source is copied here; this file only calls it.
 #include <cstring>
 #include <exception>

@@ -32,7 +32,7 @@ long sgo_schedule(long requested_steps, int b, int n, int substeps, long* flat_l
 /* ---------------------------------------------------------------- setup -- */
 
 static void vortex_spec(double gamma, double* s /* alpha mach R sigma beta L */) {
-    /* physics.cpp:234-245 VortexSpec::standard */
+    /* physics.cpp:28-39 VortexSpec::standard */
     s[0] = kPi / 4.0;
     s[1] = sqrt(2.0 / gamma);
     s[2] = 1.0;
@@ -42,7 +42,7 @@ static void vortex_spec(double gamma, double* s /* alpha mach R sigma beta L */)
 }
 
 static int vortex_state(double x, double y, const double* s, double gamma, double* q) {
-    /* physics.cpp:364-380 */
+    /* physics.cpp:158-174 */
     const double R = s[2], sigma = s[3];
     const double f = -0.5 / (sigma * sigma) * ((x / R) * (x / R) + (y / R) * (y / R));
     const double omega = s[4] * exp(f);
@@ -64,7 +64,7 @@ static int vortex_state(double x, double y, const double* s, double gamma, doubl
 }
 
 int sgo_pressure(const double* q, double gamma, double* pout) {
-    /* physics.cpp:258-267 */
+    /* physics.cpp:52-61 */
     const double rho = q[0];
     if (!(rho > 0.0)) return SGO_ENONPHYS;
     const double p = (gamma - 1.0) * (q[3] - 0.5 * (q[1] * q[1] + q[2] * q[2]) / rho);
@@ -81,7 +81,7 @@ int sgo_setup(int problem, int nx, int ny, double heat_alpha, double heat_fourie
         const double dt = heat_fourier * dx * dx / heat_alpha;
         for (int y = 0; y < ny; ++y)
             for (int x = 0; x < nx; ++x) {
-                /* xpos/ypos engine.hpp:25-26; heat_analytic physics.cpp:253-256 */
+                /* xpos/ypos engine.hpp:25-26; heat_analytic physics.cpp:47-50 */
                 const double px = 0.0 + (x + 0.0) * dx, py = 0.0 + (y + 0.0) * dy;
                 initial[(long)y * nx + x] = sin(2.0 * kPi * px) * sin(2.0 * kPi * py) *
                                             exp(-8.0 * kPi * kPi * heat_alpha * 0.0);
@@ -96,7 +96,7 @@ int sgo_setup(int problem, int nx, int ny, double heat_alpha, double heat_fourie
     const double L = s[5];
     const double dx = 2.0 * L / nx, dy = 2.0 * L / ny;
     const long plane = (long)nx * ny;
-    for (int j = 0; j < ny; ++j) { /* vortex_init physics.cpp:382-397 */
+    for (int j = 0; j < ny; ++j) { /* vortex_init physics.cpp:176-191 */
         const double y = -L + (j + 0.5) * dy;
         for (int i = 0; i < nx; ++i) {
             const double x = -L + (i + 0.5) * dx;
@@ -152,7 +152,7 @@ static inline double heat_point(const view_t* in, int x, int y, const double* hp
 
 static void minmod(const double* qm1, const double* q0, const double* qp1, const double* qp2,
                    double pm1, double p0, double pp1, double pp2, double* ql, double* qr) {
-    /* physics.cpp:281-298 */
+    /* physics.cpp:75-92 */
     const double ratio = (pp1 - p0) / (p0 - pm1);
     if (isfinite(ratio) && ratio > 0.0) {
         const double w = 0.5 * ((1.0 < ratio) ? 1.0 : ratio); /* std::min(ratio, 1.0) */
@@ -174,7 +174,7 @@ void sgo_minmod(const double* q, const double* p, double* ql, double* qr) {
 }
 
 static void flux(const double* q, int axis, double gamma, double p, double* f) {
-    /* euler_flux_x / euler_flux_y, physics.cpp:269-279 */
+    /* euler_flux_x / euler_flux_y, physics.cpp:63-73 */
     if (axis == 0) {
         const double u = q[1] / q[0];
         f[0] = q[1];
@@ -191,7 +191,7 @@ static void flux(const double* q, int axis, double gamma, double p, double* f) {
 }
 
 static int iflux(const double* ql, const double* qr, int axis, double gamma, double* f) {
-    /* interface_flux, physics.cpp:300-313 */
+    /* interface_flux, physics.cpp:94-107 */
     double pl, pr;
     if (sgo_pressure(ql, gamma, &pl) || sgo_pressure(qr, gamma, &pr)) return SGO_ENONPHYS;
     const double unl = (axis == 0 ? ql[1] : ql[2]) / ql[0];
@@ -211,7 +211,7 @@ int sgo_interface_flux(const double* ql, const double* qr, int axis, double gamm
 }
 
 static int rflux(const view_t* g, int x, int y, int axis, double gamma, double* f) {
-    /* reconstructed_flux_x/y, physics.cpp:315-335 */
+    /* reconstructed_flux_x/y, physics.cpp:109-129 */
     double q[4][4], p[4];
     for (int i = 0; i < 4; ++i) {
         const int xx = axis == 0 ? x - 1 + i : x, yy = axis == 0 ? y : y - 1 + i;
@@ -225,7 +225,7 @@ static int rflux(const view_t* g, int x, int y, int axis, double gamma, double* 
 
 static int euler_point(const view_t* base, const view_t* src, int x, int y, int stage,
                        const double* ep, double* out) {
-    /* euler_predictor_point / euler_corrector_point, physics.cpp:337-362 */
+    /* euler_predictor_point / euler_corrector_point, physics.cpp:131-156 */
     double fe[4], fw[4], gn[4], gs[4];
     int err = rflux(src, x, y, 0, ep[0], fe) | rflux(src, x - 1, y, 0, ep[0], fw) |
               rflux(src, x, y, 1, ep[0], gn) | rflux(src, x, y - 1, 1, ep[0], gs);
@@ -255,7 +255,7 @@ static int rect_step(int problem, int stage, const view_t* r1, const view_t* r2,
                 out[(long)wy * nx + wx] = heat_point(r1, x, y, params);
             } else {
                 double q[4];
-                /* physics.cpp:440-443: corrector base = read2 (Q^n), fluxes from read1 */
+                /* physics.cpp:234-237: corrector base = read2 (Q^n), fluxes from read1 */
                 err |= euler_point(stage == 0 ? r1 : r2, r1, x, y, stage, params, q);
                 for (int v = 0; v < nvars; ++v) out[((long)v * ny + wy) * nx + wx] = q[v];
             }
@@ -265,7 +265,7 @@ static int rect_step(int problem, int stage, const view_t* r1, const view_t* r2,
 
 int sgo_substep(int problem, int stage, const double* read1, const double* read2, double* out,
                 int nvars, int nx, int ny, const int* rects, int nrects, const double* params) {
-    /* run_substep_serial, physics.cpp:551-556 */
+    /* run_substep_serial, physics.cpp:345-350 */
     view_t r1 = {read1, nvars, nx, ny, 0}, r2 = {read2, nvars, nx, ny, 0};
     int err = 0;
     for (int i = 0; i < nrects; ++i)

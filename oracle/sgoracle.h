@@ -29,7 +29,7 @@ long sgo_schedule(long requested_steps, int b, int n, int substeps, long* flat_l
 int sgo_setup(int problem, int nx, int ny, double heat_alpha, double heat_fourier,
               double gamma, double cfl, double* initial, double* dt_dx_dy);
 
-/* physics.hpp:57-63 / physics.cpp:337-362 applied on rectangles; the grid wraps
+/* physics.hpp:57-63 / physics.cpp:131-156 applied on rectangles; the grid wraps
  * in y (field.hpp:18-21); x must be in range.  rects: n x {x0,x1,y0,y1}.
  * params: heat {alpha,dx,dy,dt}; euler {gamma,dx,dy,dt}. */
 int sgo_substep(int problem, int stage, const double* read1, const double* read2, double* out,
@@ -48,7 +48,7 @@ int sgo_standard_solve(int problem, int nx, int ny, long levels, const double* p
 int sgo_swept_solve(int problem, int nx, int ny, int b, long octahedra, long out_level,
                     const double* params, const double* initial, double* out);
 
-/* physics.cpp:258-313 known-answer helpers */
+/* physics.cpp:52-107 known-answer helpers */
 int sgo_pressure(const double* q, double gamma, double* p);
 void sgo_minmod(const double* q4x4, const double* p4, double* ql, double* qr);
 int sgo_interface_flux(const double* ql, const double* qr, int axis, double gamma, double* f);

@@ -43,6 +43,7 @@ class sg_result(C.Structure):
         ("modeled_seconds", C.c_double), ("messages", C.c_long), ("bytes", C.c_longlong),
         ("cell_updates", C.c_longlong), ("snapshot_frames", C.c_long), ("kernel_launches", C.c_long),
         ("final_field", C.POINTER(C.c_double)),
+        ("nparts", C.c_int), ("part_messages", C.POINTER(C.c_long)), ("part_bytes", C.POINTER(C.c_longlong)),
     ]
 
 

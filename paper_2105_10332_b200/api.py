@@ -258,6 +258,8 @@ class RunRecord:  # engine.hpp:35-59
     solve_seconds: float = 0.0
     kernel_launches: int = 0
     final_level: int = 0
+    part_messages: list = field(default_factory=list)
+    part_bytes: list = field(default_factory=list)
 
     def to_json(self, gpu_extras: bool = False) -> dict:
         """engine.cpp:461-491 key set and order."""
@@ -265,9 +267,12 @@ class RunRecord:  # engine.hpp:35-59
             "engine", "problem", "mode", "nx", "block", "ranks", "steps_requested", "actual_steps",
             "total_levels", "octahedra", "communicates", "dt", "setup_seconds", "wall_seconds",
             "modeled_seconds", "messages", "bytes", "cell_updates", "snapshot_frames")}
-        per = max(1, self.ranks)
-        j["per_rank"] = [{"messages": self.messages // per, "bytes": self.bytes // per, "comm_seconds": 0.0,
-                          "compute_seconds": 0.0, "clock": 0.0} for _ in range(per)]
+        # per_rank (engine.cpp:482-489): one entry per partition = rank, the
+        # pushes it made into other partitions; the virtual clocks are 0
+        pm = self.part_messages or [0] * max(1, self.ranks)
+        pb = self.part_bytes or [0] * max(1, self.ranks)
+        j["per_rank"] = [{"messages": int(m), "bytes": int(b), "comm_seconds": 0.0, "compute_seconds": 0.0,
+                          "clock": 0.0} for m, b in zip(pm, pb)]
         if gpu_extras:
             j.update(ny=self.ny, px=self.px, py=self.py, solve_seconds=self.solve_seconds,
                      kernel_launches=self.kernel_launches, final_level=self.final_level)
@@ -290,7 +295,9 @@ def _result(r: _c.sg_result) -> RunResult:
         setup_seconds=r.setup_seconds, wall_seconds=r.wall_seconds, modeled_seconds=r.modeled_seconds,
         messages=r.messages, bytes=r.bytes, cell_updates=r.cell_updates, snapshot_frames=r.snapshot_frames,
         ny=r.ny, px=r.px, py=r.py, solve_seconds=r.solve_seconds, kernel_launches=r.kernel_launches,
-        final_level=r.final_level)
+        final_level=r.final_level,
+        part_messages=[int(r.part_messages[q]) for q in range(r.nparts)] if r.part_messages else [],
+        part_bytes=[int(r.part_bytes[q]) for q in range(r.nparts)] if r.part_bytes else [])
     return RunResult(FieldState(r.nvars, r.nx, r.ny, r.final_level, data), rec)
 
 
@@ -383,20 +390,21 @@ class Solver:
         finally:
             self._L.sg_free_result(C.byref(res))
 
-    def _piece_shape(self):
-        """(nvars, rows, cols) of the host arrays upload/download/initial take:
-        the global field, or this rank's partition piece in a distributed run."""
+    def _piece_shape(self, whole: bool = False):
+        """(nvars, rows, cols) of the host arrays upload/download take: the
+        global field, or this rank's partition piece in a distributed run
+        (initial() always writes the whole global field: whole=True)."""
         c = self._cfg
         nv = 1 if c.problem == _c.SG_HEAT else 4
         ny = c.ny if c.ny > 0 else c.nx
-        if getattr(self, "_dist", None) is None:
+        if whole or getattr(self, "_dist", None) is None:
             return nv, ny, c.nx
         px = c.px if c.px > 0 else (c.ranks if c.py <= 0 else 1)
         py = c.py if c.py > 0 else 1
         return nv, ny // py, c.nx // px
 
     def _host_ptr(self, host, what: str) -> C.c_void_p:
-        return C.c_void_p(_host_f64_ptr(host, self._piece_shape(), what))
+        return C.c_void_p(_host_f64_ptr(host, self._piece_shape(whole=what == "initial"), what))
 
     def upload(self, host) -> None:
         """Replace level 0 from a host array [var][ny][nx] float64 (numpy, or a
@@ -410,7 +418,8 @@ class Solver:
         _check(self._L.sg_solver_download(self._h, self._host_ptr(host, "download"), err, len(err)), err)
 
     def initial(self, host) -> None:
-        """The initial condition make_setup computed (engine.cpp:27-70) into a host array."""
+        """The initial condition make_setup computed (engine.cpp:27-70) into a
+        host array of the global field's shape (also in a distributed run)."""
         err = _c.errbuf()
         _check(self._L.sg_solver_initial(self._h, self._host_ptr(host, "initial"), err, len(err)), err)
 

@@ -192,7 +192,12 @@ int sg_run(const sg_config* cfg, sg_result* out, char* err, size_t errlen) {
 void sg_free_result(sg_result* r) {
     if (!r) return;
     std::free(r->final_field);
+    std::free(r->part_messages);
+    std::free(r->part_bytes);
     r->final_field = nullptr;
+    r->part_messages = nullptr;
+    r->part_bytes = nullptr;
+    r->nparts = 0;
 }
 
 double sg_measure_fp64_peak(void) { return sg::measure_fp64_peak(); }
@@ -233,7 +238,7 @@ int sg_substep(int problem, int stage, const double* d_read1, const double* d_re
             c[0] = params[0] * params[3] / (params[1] * params[1]);
             c[1] = params[0] * params[3] / (params[2] * params[2]);
             c[2] = c[3] = 0.0;
-        } else {  // params {gamma, dx, dy, dt}; physics.cpp:342-343, 356-357
+        } else {  // params {gamma, dx, dy, dt}; physics.cpp:136-137, 150-151
             c[0] = params[0];
             c[1] = stage == 0 ? 0.5 * params[3] / params[1] : params[3] / params[1];
             c[2] = stage == 0 ? 0.5 * params[3] / params[2] : params[3] / params[2];

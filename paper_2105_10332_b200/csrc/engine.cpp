@@ -235,9 +235,14 @@ void Solver::build_swept() {
                             sizeof(double) * pw_);
         ck(cudaMemcpy(pb.init, piece.data(), piece.size() * sizeof(double), cudaMemcpyHostToDevice), "init H2D");
     }
-    // ledger: record pushes across partition boundaries (P2P / NVLink stores)
-    long pushes = 0;
-    for (const auto& pb : parts_)
+    // ledger: record pushes across partition boundaries (P2P / NVLink stores),
+    // per partition: the instances whose record lands in another partition's
+    // ghost ring, and the distinct partitions one launch pushes into
+    part_messages_.assign(nparts_, 0);
+    part_bytes_.assign(nparts_, 0);
+    for (const auto& pb : parts_) {
+        long pushes = 0;
+        std::vector<char> peer(nparts_, 0);
         for (int bj = 0; bj < pby; ++bj)
             for (int bi = 0; bi < pbx; ++bi)
                 for (int ej = -1; ej <= 1; ++ej)
@@ -246,12 +251,22 @@ void Solver::build_swept() {
                         const int tbi = bi - ei * pbx, tbj = bj - ej * pby;
                         if (tbi < -g || tbi >= pbx + g || tbj < -g || tbj >= pby + g) continue;
                         const int tp = ((pb.pj + ej + py_) % py_) * px_ + (pb.pi + ei + px_) % px_;
-                        if (tp != pb.id) ++pushes;
+                        if (tp != pb.id) {
+                            ++pushes;
+                            peer[tp] = 1;
+                        }
                     }
-    for (const Launch& l : P.launches) {
-        if (P.kinds[l.kind].epad == 0) continue;
-        bytes_ += static_cast<long long>(pushes) * P.kinds[l.kind].exp_cells.size() * nv * 8;
-        if (pushes) messages_ += nparts_;
+        long npeers = 0;
+        for (char c : peer) npeers += c;
+        for (const Launch& l : P.launches) {
+            if (P.kinds[l.kind].epad == 0) continue;
+            part_bytes_[pb.id] += static_cast<long long>(pushes) * P.kinds[l.kind].exp_cells.size() * nv * 8;
+            part_messages_[pb.id] += npeers;
+        }
+    }
+    for (int q = 0; q < nparts_; ++q) {
+        bytes_ += part_bytes_[q];
+        messages_ += part_messages_[q];
     }
 }
 
@@ -472,18 +487,22 @@ void Solver::build_standard() {
         ck(cudaMemcpy(pb.init_ghosted, piece.data(), piece.size() * sizeof(double), cudaMemcpyHostToDevice),
            "init H2D");
     }
-    // ledger: 4 face strips per partition per level when neighbours differ
-    for (long l = 1; l <= final_level_; ++l)
-        for (int q = 0; q < nparts_; ++q) {
-            if (px_ > 1) {
-                messages_ += 2;
-                bytes_ += 2LL * ph_ * n * nv * 8;
-            }
-            if (py_ > 1) {
-                messages_ += 2;
-                bytes_ += 2LL * pw_ * n * nv * 8;
-            }
+    // ledger: per level, each partition pushes its n-wide face strips into
+    // the face neighbours that are other partitions
+    part_messages_.assign(nparts_, 0);
+    part_bytes_.assign(nparts_, 0);
+    for (int q = 0; q < nparts_; ++q) {
+        if (px_ > 1) {
+            part_messages_[q] += 2 * final_level_;
+            part_bytes_[q] += 2LL * ph_ * n * nv * 8 * final_level_;
         }
+        if (py_ > 1) {
+            part_messages_[q] += 2 * final_level_;
+            part_bytes_[q] += 2LL * pw_ * n * nv * 8 * final_level_;
+        }
+        messages_ += part_messages_[q];
+        bytes_ += part_bytes_[q];
+    }
     prof_kind_ = 100;  // std step
 }
 
@@ -965,6 +984,13 @@ void Solver::fetch(sg_result* r) {
     r->kernel_launches = launches_;
     r->snapshot_frames = snapshot_frames_;
     r->final_field = field;
+    r->nparts = nparts_;
+    r->part_messages = static_cast<long*>(std::malloc(sizeof(long) * nparts_));
+    r->part_bytes = static_cast<long long*>(std::malloc(sizeof(long long) * nparts_));
+    for (int q = 0; q < nparts_; ++q) {
+        r->part_messages[q] = q < static_cast<int>(part_messages_.size()) ? part_messages_[q] : 0;
+        r->part_bytes[q] = q < static_cast<int>(part_bytes_.size()) ? part_bytes_[q] : 0;
+    }
 }
 
 void Solver::upload(const double* host) {

@@ -101,6 +101,8 @@ class Solver {
     long long cell_updates_ = 0;
     long messages_ = 0;
     long long bytes_ = 0;
+    std::vector<long> part_messages_;       // per partition (ledger per rank)
+    std::vector<long long> part_bytes_;
     long launches_ = 0;
     std::vector<PartBuffers> parts_;
     std::vector<DeviceCtx> devs_;

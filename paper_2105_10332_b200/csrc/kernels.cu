@@ -19,7 +19,7 @@
 //      neighbours' ghost frames (StandardRank::exchange_ghosts + compute,
 //      engine.cpp:351-408 of the reference).  std_step_kernel<PROB> is the
 //      point-wise fallback for odd partition widths.
-//  substep_rects_kernel<PROB>: run_substep on rectangles (physics.cpp:551-575).
+//  substep_rects_kernel<PROB>: run_substep on rectangles (physics.cpp:345-369).
 //  dist_barrier_kernel: cross-process launch ordering (one process per GPU).
 //  fp64_peak_kernel: DADD+DMUL microbenchmark for the FP64 roofline.
 #include <cuda_runtime.h>

@@ -620,6 +620,22 @@ std::string describe_plan(const SweptPlan& p) {
            << " init " << T.inits.size() << " segs";
         for (const Segment& s : T.segs)
             os << " [d" << s.delta << " " << s.di << "," << s.dj << " " << kind_name(s.pkind) << "]";
+        {  // contiguous record runs per producer (what one bulk copy each could move)
+            std::map<int, std::vector<int>> by;
+            for (const Import& x : T.imports) by[x.seg].push_back(x.src);
+            long runs = 0, cells16 = 0;
+            for (auto& kv : by) {
+                std::sort(kv.second.begin(), kv.second.end());
+                for (std::size_t i = 0; i < kv.second.size();) {
+                    std::size_t j = i;
+                    while (j + 1 < kv.second.size() && kv.second[j + 1] == kv.second[j] + 1) ++j;
+                    ++runs;
+                    cells16 += ((kv.second[j] + 2) & ~1) - (kv.second[i] & ~1);
+                    i = j + 1;
+                }
+            }
+            os << " runs " << runs << " cells16 " << cells16;
+        }
         os << "\n";
     }
     return os.str();

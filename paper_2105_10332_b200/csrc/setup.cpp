@@ -128,7 +128,7 @@ void validate(const sg_config& c) {
 
 namespace {
 
-// VortexSpec::standard, physics.cpp:234-245: {alpha, mach, R, sigma, beta, L}
+// VortexSpec::standard, physics.cpp:28-39: {alpha, mach, R, sigma, beta, L}
 struct Vortex {
     double alpha, mach, radius, sigma, beta, half_extent;
 };
@@ -143,7 +143,7 @@ Vortex vortex_standard(double gamma) {
     return s;
 }
 
-// vortex_state, physics.cpp:364-380
+// vortex_state, physics.cpp:158-174
 void vortex_state(double x, double y, const Vortex& s, double gamma, double* q) {
     const double f = -0.5 / (s.sigma * s.sigma) *
                      ((x / s.radius) * (x / s.radius) + (y / s.radius) * (y / s.radius));
@@ -164,7 +164,7 @@ void vortex_state(double x, double y, const Vortex& s, double gamma, double* q) 
     q[3] = e;
 }
 
-double pressure_host(const double* q, double gamma) {  // physics.cpp:258-267
+double pressure_host(const double* q, double gamma) {  // physics.cpp:52-61
     const double rho = q[0];
     if (!(rho > 0.0)) fail(SG_ENONPHYS, "non-physical state: rho <= 0");
     const double p = (gamma - 1.0) * (q[3] - 0.5 * (q[1] * q[1] + q[2] * q[2]) / rho);
@@ -184,7 +184,7 @@ Setup make_setup(const sg_config& c) {
     const std::size_t plane = static_cast<std::size_t>(nx) * ny;
     s.initial.assign(plane * s.eq.nvars, 0.0);
     if (c.problem == SG_HEAT) {
-        // engine.cpp:31-42; heat_analytic physics.cpp:253-256 at node positions
+        // engine.cpp:31-42; heat_analytic physics.cpp:47-50 at node positions
         s.dx = 1.0 / nx;
         s.dy = 1.0 / ny;
         s.dt = c.heat_fourier * s.dx * s.dx / c.heat_alpha;
@@ -199,7 +199,7 @@ Setup make_setup(const sg_config& c) {
         s.heat_fx = c.heat_alpha * s.dt / (s.dx * s.dx);
         s.heat_fy = c.heat_alpha * s.dt / (s.dy * s.dy);
     } else {
-        // engine.cpp:43-68; vortex_init physics.cpp:382-397 (cell centred)
+        // engine.cpp:43-68; vortex_init physics.cpp:176-191 (cell centred)
         const Vortex v = vortex_standard(c.gamma);
         const double L = v.half_extent;
         s.dx = 2.0 * L / nx;

@@ -19,7 +19,7 @@ struct Error : std::runtime_error {
 
 // ------------------------------------------------------------- problem --
 // Equation plugin metadata: StencilShape::heat/euler (geometry.cpp:8-24),
-// nvars_for (physics.cpp:232).
+// nvars_for (physics.cpp:26).
 struct Equation {
     int problem = SG_HEAT;
     int nvars = 1;
@@ -35,7 +35,7 @@ struct Setup {
     int nx = 0, ny = 0;
     double dx = 0, dy = 0, dt = 0;
     // Kernel coefficients precomputed with the reference's association
-    // order (physics.hpp:58-59, physics.cpp:342-343,356-357).
+    // order (physics.hpp:58-59, physics.cpp:136-137,150-151).
     double heat_fx = 0, heat_fy = 0;          // (alpha*dt)/(dx*dx)
     double gamma = 1.4;
     double cx_pred = 0, cy_pred = 0;          // (0.5*dt)/dx

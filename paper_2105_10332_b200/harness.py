@@ -5,7 +5,7 @@
     run_weak_scaling(spec, csv_path)   bench.cpp:208-244
     run_verify(problem, sizes)         bench.cpp:246-310
 Solver numerics all run on the GPU through run(); only the analytic reference
-fields (heat_analytic / vortex_analytic, physics.cpp:253-256, 399-422) are
+fields (heat_analytic / vortex_analytic, physics.cpp:47-50, 193-216) are
 evaluated here with numpy to measure errors (tolerances ~1e-4, not parity).
 """
 from __future__ import annotations
@@ -122,11 +122,11 @@ def run_weak_scaling(spec: SweepSpec, csv_path: str, log=None) -> None:
 
 
 # ----------------------------------------------------------------- verify --
-def heat_analytic(x, y, t, alpha):  # physics.cpp:253-256
+def heat_analytic(x, y, t, alpha):  # physics.cpp:47-50
     return np.sin(2.0 * np.pi * x) * np.sin(2.0 * np.pi * y) * np.exp(-8.0 * np.pi * np.pi * alpha * t)
 
 
-def vortex_analytic(nx, ny, gamma, t):  # physics.cpp:399-422 (VortexSpec::standard, :234-245)
+def vortex_analytic(nx, ny, gamma, t):  # physics.cpp:193-216 (VortexSpec::standard, :28-39)
     mach = math.sqrt(2.0 / gamma)
     alpha = math.pi / 4.0
     beta = mach * (5.0 * math.sqrt(2.0) / (4.0 * math.pi)) * math.exp(0.5)
