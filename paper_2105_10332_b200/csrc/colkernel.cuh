@@ -1,0 +1,485 @@
+// Register-tile heat phase kernel (swept_heat_col_kernel) and its launcher,
+// instantiated once per block size in kernels_col<B>.cu so the five block
+// sizes compile in parallel.
+#pragma once
+
+#include "colgeom.hpp"
+#include "devutil.cuh"
+#include "physics.cuh"
+
+namespace sg {
+namespace {
+
+// Heat phase kernel, register-tile form (block B in {8, 16, 32}, geometry in
+// colgeom.hpp).  L = B/CPL lanes own one phase instance (32/L instances per
+// warp, WPC warps per CTA).  At each level the instance's B x B window lives
+// in the lanes' registers, in one of two layouts (col::mode):
+//   COL: lane l holds columns c = CPL*l + q, v[q][i] = row ylo + i;
+//   ROW: lane l holds rows ylo + CPL*l + q, v[q][x] = column x.
+// The bridges switch layout once (a transpose through shared memory) so that
+// every level iterates over the shorter side of its rectangle.  Per level r
+// (geometry compile-time, levels and cells fully unrolled):
+//   1. imports: cells of level r-1 this instance did not compute come from
+//      shared memory, where the gather landed them (predicated LDS);
+//   2. update R_r in place: neighbours along a lane's lines and between its
+//      own CPL lines are registers; across lanes they come from lanes +-1 by
+//      warp shuffle, one 64-bit shuffle each way per CPL lines (heat_point,
+//      physics.hpp:57-63; no FMA);
+//   3. exports: the cells of R_r that other instances read go from registers
+//      into this instance's record (predicated stores).
+// Lanes outside R_r compute too (SIMT); their cells are never read before an
+// import overwrites them.
+template <int B, int KIND, int CPL, int WPC>
+__global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_constant__ SweptArgs A) {
+    constexpr int L = B / CPL;      // lanes per instance
+    constexpr int IPW = 32 / L;     // instances per warp
+    constexpr int IPC = WPC * IPW;  // instances per CTA
+    constexpr int NL = col::nlev(KIND, B);
+    constexpr int YLO = col::ylo(KIND, B);
+    constexpr int NIMP = col::imp_total(KIND, B);  // import slots; the transpose tile follows
+    extern __shared__ double sm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // b = 12 / 24: the last 32 - IPW*L lanes of a warp are dead (they run the
+    // code, shuffles included, but never write anything)
+    const bool dead = lane >= IPW * L;
+    const int sub = dead ? 0 : lane / L, l = lane % L;
+    const int slot_in_cta = warp * IPW + sub;
+    const int ninst = A.pbx * A.pby;
+    // odd launches walk the instances backwards: their first CTAs read the
+    // records the previous launch wrote last (still in L2)
+    const int cta = (A.lo_parity & 1) ? gridDim.x - 1 - blockIdx.x : blockIdx.x;
+    const int inst = cta * IPC + slot_in_cta;
+    const bool live = !dead && inst < ninst;
+    const int part = A.dev_parts[blockIdx.y];
+    const int pi = part % A.px, pj = part / A.px;
+    const int bi = live ? inst % A.pbx : 0, bj = live ? inst / A.pbx : 0;
+    const int half = A.frame * (B / 2);
+    const int gh = A.ghost;
+    double* S = sm + slot_in_cta * A.smem_doubles;
+
+    // ---- gather the imports: {offset from this instance's slot-0 record, smem slot}
+    if (live) {
+        const double* ibase = A.rec[part * A.nslots] + ((long)(bj + gh) * A.extw + (bi + gh)) * A.epad;
+        // part A (levels <= gather_split), one cp.async group, then part B
+        const int na = A.nimp - A.nimp_b;
+        int i = l;
+        for (; i + 3 * L < na; i += 4 * L) {
+            const int2 e0 = ldg_keep(&A.imp_off[i]), e1 = ldg_keep(&A.imp_off[i + L]);
+            const int2 e2 = ldg_keep(&A.imp_off[i + 2 * L]), e3 = ldg_keep(&A.imp_off[i + 3 * L]);
+            cp_async8(S + e0.y, ibase + e0.x);
+            cp_async8(S + e1.y, ibase + e1.x);
+            cp_async8(S + e2.y, ibase + e2.x);
+            cp_async8(S + e3.y, ibase + e3.x);
+        }
+        for (; i < na; i += L) {
+            const int2 e = ldg_keep(&A.imp_off[i]);
+            cp_async8(S + e.y, ibase + e.x);
+        }
+        cp_async_commit();
+        i = na + l;
+        for (; i + 3 * L < A.nimp; i += 4 * L) {
+            const int2 e0 = ldg_keep(&A.imp_off[i]), e1 = ldg_keep(&A.imp_off[i + L]);
+            const int2 e2 = ldg_keep(&A.imp_off[i + 2 * L]), e3 = ldg_keep(&A.imp_off[i + 3 * L]);
+            cp_async8(S + e0.y, ibase + e0.x);
+            cp_async8(S + e1.y, ibase + e1.x);
+            cp_async8(S + e2.y, ibase + e2.x);
+            cp_async8(S + e3.y, ibase + e3.x);
+        }
+        for (; i < A.nimp; i += L) {
+            const int2 e = ldg_keep(&A.imp_off[i]);
+            cp_async8(S + e.y, ibase + e.x);
+        }
+        for (int j = l; j < A.ninit; j += L) {
+            const int4 im = __ldg(&A.inits[j]);
+            const int gx = wrapi(pi * A.pw + bi * B - half + im.x, A.nx);
+            const int gy = wrapi(pj * A.ph + bj * B - half + im.y, A.ny);
+            const int opi = gx / A.pw, opj = gy / A.ph;
+            S[im.z] = A.init_planes[opj * A.px + opi][(long)(gy - opj * A.ph) * A.pw + (gx - opi * A.pw)];
+        }
+    }
+    cp_async_commit();
+    cp_async_wait_group<1>();  // part A (part B may still be in flight)
+    __syncwarp();
+
+    double* dst = A.rec[part * A.nslots + A.my_slot] + ((long)(bj + gh) * A.extw + (bi + gh)) * A.epad;
+    const double fx = A.c0, fy = A.c1;
+    const unsigned s_imp = static_cast<unsigned>(__cvta_generic_to_shared(S));
+    double* tile = S + NIMP;
+    // output stash (only allocated by launches that write the output level or snapshots)
+    double* stash = sm + IPC * A.smem_doubles + (slot_in_cta * L + l) * CPL * B;
+    double v[CPL][B];
+#pragma unroll
+    for (int q = 0; q < CPL; ++q)
+#pragma unroll
+        for (int i = 0; i < B; ++i) v[q][i] = 0.0;
+
+    sfor<NL>([&](auto RI) {
+        constexpr int r = decltype(RI)::value + 1;
+        constexpr int MODE = col::mode(KIND, B, r);
+        constexpr col::CRect q0 = col::rect(KIND, B, r);
+        if constexpr (r == col::gather_split(KIND, B) + 1) {
+            cp_async_wait_all();  // part B
+            __syncwarp();
+        }
+        // ---------------- 1. imports of level r-1
+        if constexpr (MODE == col::COL) {
+            bool ip[CPL][4];
+            unsigned ia[CPL][4];
+            sfor<4>([&](auto TI) {
+                constexpr int t = decltype(TI)::value;
+                constexpr col::RowSet ts = col::Geo<KIND, B>::t.imp_tset[r][t];
+#pragma unroll
+                for (int q = 0; q < CPL; ++q) {
+                    const int c = CPL * l + q;
+                    ip[q][t] = ts.count() > 0 && ts.has(c);
+                    ia[q][t] = s_imp + 8u * static_cast<unsigned>(ts.count() > 0 ? ts.rank(c) : 0);
+                }
+            });
+            sfor<B>([&](auto YI) {
+                constexpr int j = decltype(YI)::value;
+                constexpr int t = col::Geo<KIND, B>::t.imp_type[r][j];
+                constexpr int base = col::Geo<KIND, B>::t.imp_base[r][j];
+                if constexpr (t >= 0) {
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) lds_if(v[q][j], ia[q][t] + 8u * base, ip[q][t]);
+                }
+            });
+        } else {
+            int myt[CPL], mybase[CPL];
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) {
+                const int i = CPL * l + q;
+                myt[q] = -1;
+                mybase[q] = 0;
+                sfor<col::kMaxRuns>([&](auto UI) {
+                    constexpr col::Run ru = col::Geo<KIND, B>::t.imp_runs[r][decltype(UI)::value];
+                    if constexpr (ru.t >= 0)
+                        if (i >= ru.i0 && i < ru.i1) {
+                            myt[q] = ru.t;
+                            mybase[q] = ru.base + (i - ru.i0) * ru.cnt;
+                        }
+                });
+            }
+            sfor<4>([&](auto TI) {
+                constexpr int t = decltype(TI)::value;
+                constexpr col::RowSet ts = col::Geo<KIND, B>::t.imp_tset[r][t];
+                if constexpr (ts.count() > 0) {
+                    sfor<B>([&](auto XI) {
+                        constexpr int x = decltype(XI)::value;
+                        constexpr col::RowSet tx = col::Geo<KIND, B>::t.imp_tset[r][t];
+                        constexpr int rk = tx.rank(x);
+                        if constexpr (tx.has(x)) {
+#pragma unroll
+                            for (int q = 0; q < CPL; ++q)
+                                lds_if(v[q][x], s_imp + 8u * static_cast<unsigned>(mybase[q] + rk), myt[q] == t);
+                        }
+                    });
+                }
+            });
+        }
+        // ---------------- 2. update R_r in place
+        if constexpr (MODE == col::COL) {
+            double prev[CPL];  // old values of the row below
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) prev[q] = v[q][q0.y0 - 1 - YLO];
+            sfor<B>([&](auto YI) {
+                constexpr int j = decltype(YI)::value;
+                constexpr col::CRect qr = col::rect(KIND, B, r);
+                if constexpr (YLO + j >= qr.y0 && YLO + j < qr.y1) {
+                    double cur[CPL];
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) cur[q] = v[q][j];
+                    const double east = __shfl_down_sync(0xffffffffu, cur[0], 1);
+                    const double west = __shfl_up_sync(0xffffffffu, cur[CPL - 1], 1);
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) {
+                        const double e = q + 1 < CPL ? cur[q + 1 < CPL ? q + 1 : 0] : east;
+                        const double w = q > 0 ? cur[q > 0 ? q - 1 : 0] : west;
+                        v[q][j] = heat_update(cur[q], e, w, v[q][j + 1], prev[q], fx, fy);
+                        prev[q] = cur[q];
+                    }
+                }
+            });
+        } else {
+            double prev[CPL];  // old values of the column to the west
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) prev[q] = v[q][q0.x0 - 1];
+            sfor<B>([&](auto XI) {
+                constexpr int x = decltype(XI)::value;
+                constexpr col::CRect qr = col::rect(KIND, B, r);
+                if constexpr (x >= qr.x0 && x < qr.x1) {
+                    double cur[CPL];
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) cur[q] = v[q][x];
+                    const double north = __shfl_down_sync(0xffffffffu, cur[0], 1);
+                    const double south = __shfl_up_sync(0xffffffffu, cur[CPL - 1], 1);
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) {
+                        const double n = q + 1 < CPL ? cur[q + 1 < CPL ? q + 1 : 0] : north;
+                        const double sv = q > 0 ? cur[q > 0 ? q - 1 : 0] : south;
+                        v[q][x] = heat_update(cur[q], v[q][x + 1], prev[q], n, sv, fx, fy);
+                        prev[q] = cur[q];
+                    }
+                }
+            });
+        }
+        // ---------------- 3. exports of level r (grouped layout, colgeom.hpp ExpLev)
+        if constexpr (col::grouped_exports(B)) if (live) {
+            constexpr col::ExpLev E = col::Geo<KIND, B>::t.exp.lev[r];
+            if constexpr (E.count() > 0) {
+                if constexpr (MODE == col::COL) {
+                    bool pb[CPL], pm[CPL];
+                    double* gh_[CPL];
+                    double* gc[CPL];
+                    double* gm[CPL];
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) {
+                        const int c = CPL * l + q;
+                        pb[q] = E.band(c);
+                        pm[q] = E.mid(c) && c >= E.x0 && c < E.x1;
+                        const int rb = pb[q] ? E.rank_band(c) : 0;
+                        gh_[q] = dst + (E.g1 + rb - E.yh0 * E.bw());  // hole rows: + y * bw
+                        gc[q] = dst + (E.g3 + rb);                     // full rows, band: + f * bw
+                        gm[q] = dst + (E.g2 + (pm[q] ? c - E.mp : 0)); // full rows, middle: + f * mw
+                    }
+                    sfor<B>([&](auto YI) {
+                        constexpr int j = decltype(YI)::value;
+                        constexpr col::ExpLev Ej = col::Geo<KIND, B>::t.exp.lev[r];
+                        constexpr int y = YLO + j;
+                        constexpr int f = Ej.full_index(y);
+                        if constexpr (Ej.hole_row(y)) {
+#pragma unroll
+                            for (int q = 0; q < CPL; ++q) stg_if(gh_[q] + y * Ej.bw(), v[q][j], pb[q]);
+                        } else if constexpr (f >= 0) {
+                            if constexpr (Ej.bw() > 0) {
+#pragma unroll
+                                for (int q = 0; q < CPL; ++q) stg_if(gc[q] + f * Ej.bw(), v[q][j], pb[q]);
+                            }
+#pragma unroll
+                            for (int q = 0; q < CPL; ++q) stg_if(gm[q] + f * Ej.mw(), v[q][j], pm[q]);
+                        }
+                    });
+                } else {
+                    bool pbr[CPL], pmr[CPL];
+                    double* gb[CPL];
+                    double* gm[CPL];
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) {
+                        const int y = YLO + CPL * l + q;  // the lane's window row
+                        const bool hole = E.hole_row(y);
+                        const int f = E.full_index(y);
+                        pbr[q] = hole || f >= 0;
+                        pmr[q] = f >= 0;
+                        gb[q] = dst + (hole ? E.g1 + (y - E.yh0) * E.bw() : E.g3 + (f >= 0 ? f : 0) * E.bw());
+                        gm[q] = dst + (E.g2 + (f >= 0 ? f : 0) * E.mw() - E.mp);
+                    }
+                    sfor<B>([&](auto XI) {
+                        constexpr int x = decltype(XI)::value;
+                        constexpr col::ExpLev Ex = col::Geo<KIND, B>::t.exp.lev[r];
+                        if constexpr (Ex.band(x)) {
+                            constexpr int rk = Ex.rank_band(x);
+#pragma unroll
+                            for (int q = 0; q < CPL; ++q) stg_if(gb[q] + rk, v[q][x], pbr[q]);
+                        } else if constexpr (Ex.mid(x) && x >= Ex.x0 && x < Ex.x1) {
+#pragma unroll
+                            for (int q = 0; q < CPL; ++q) stg_if(gm[q] + x, v[q][x], pmr[q]);
+                        }
+                    });
+                }
+            }
+        }
+        // b = 32: row-major record (colgeom.hpp grouped_exports)
+        if constexpr (!col::grouped_exports(B)) if (live) {
+            if constexpr (MODE == col::COL) {
+                bool ep[CPL][2];
+                double* eg[CPL][2];
+                sfor<2>([&](auto TI) {
+                    constexpr int t = decltype(TI)::value;
+                    constexpr col::RowSet ts = col::Geo<KIND, B>::t.exp_tset[r][t];
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) {
+                        const int c = CPL * l + q;
+                        ep[q][t] = ts.count() > 0 && ts.has(c);
+                        eg[q][t] = dst + (ts.count() > 0 ? ts.rank(c) : 0);
+                    }
+                });
+                sfor<B>([&](auto YI) {
+                    constexpr int j = decltype(YI)::value;
+                    constexpr int t = col::Geo<KIND, B>::t.exp_type[r][j];
+                    constexpr int base = col::Geo<KIND, B>::t.exp_base[r][j];
+                    static_assert(t < 2, "export row types");
+                    if constexpr (t >= 0) {
+#pragma unroll
+                        for (int q = 0; q < CPL; ++q) stg_if(eg[q][t] + base, v[q][j], ep[q][t]);
+                    }
+                });
+            } else {
+                int myt[CPL];
+                double* eb[CPL];
+#pragma unroll
+                for (int q = 0; q < CPL; ++q) {
+                    const int i = CPL * l + q;
+                    myt[q] = -1;
+                    int mybase = 0;
+                    sfor<col::kMaxRuns>([&](auto UI) {
+                        constexpr col::Run ru = col::Geo<KIND, B>::t.exp_runs[r][decltype(UI)::value];
+                        if constexpr (ru.t >= 0)
+                            if (i >= ru.i0 && i < ru.i1) {
+                                myt[q] = ru.t;
+                                mybase = ru.base + (i - ru.i0) * ru.cnt;
+                            }
+                    });
+                    eb[q] = dst + mybase;
+                }
+                sfor<2>([&](auto TI) {
+                    constexpr int t = decltype(TI)::value;
+                    constexpr col::RowSet ts = col::Geo<KIND, B>::t.exp_tset[r][t];
+                    if constexpr (ts.count() > 0) {
+                        sfor<B>([&](auto XI) {
+                            constexpr int x = decltype(XI)::value;
+                            constexpr col::RowSet tx = col::Geo<KIND, B>::t.exp_tset[r][t];
+                            constexpr int rk = tx.rank(x);
+                            if constexpr (tx.has(x)) {
+#pragma unroll
+                                for (int q = 0; q < CPL; ++q) stg_if(eb[q] + rk, v[q][x], myt[q] == t);
+                            }
+                        });
+                    }
+                });
+            }
+        }
+        // ---------------- output level / snapshot (rare): through the lane's
+        // shared-memory stash to a non-inlined writer
+        if ((((A.out_mask | A.snap_mask) >> r) & 1ull) && !dead) {
+#pragma unroll
+            for (int q = 0; q < CPL; ++q)
+#pragma unroll
+                for (int i = 0; i < B; ++i) stash[q * B + i] = v[q][i];
+            const long lev = A.lo + r - 1;
+            const bool o = (A.out_mask >> r) & 1ull, sn = (A.snap_mask >> r) & 1ull;
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) {
+                const int m = CPL * l + q;  // the lane's column (COL) or window row (ROW)
+                if constexpr (MODE == col::COL) {
+                    if (live && m >= q0.x0 && m < q0.x1)
+                        put_cells(A, stash + q * B, q0.y0 - YLO, q0.y1 - YLO, pi, pj, bi * B - half + m,
+                                  bj * B - half + YLO, 0, 1, lev, o, sn);
+                } else {
+                    if (live && YLO + m >= q0.y0 && YLO + m < q0.y1)
+                        put_cells(A, stash + q * B, q0.x0, q0.x1, pi, pj, bi * B - half, bj * B - half + YLO + m, 1,
+                                  0, lev, o, sn);
+                }
+            }
+        }
+        // ---------------- layout switch after this level: transpose R_r
+        if constexpr (r < NL && col::mode(KIND, B, r + 1) != MODE) {
+            constexpr int w = q0.x1 - q0.x0;
+            static_assert(w * (q0.y1 - q0.y0) <= col::tile_doubles(KIND, B), "transpose tile");
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) {
+                const int m = CPL * l + q;
+                if constexpr (MODE == col::COL) {
+                    if (!dead && m >= q0.x0 && m < q0.x1) {
+                        double* t0 = tile + (m - q0.x0);
+                        sfor<B>([&](auto YI) {
+                            constexpr int j = decltype(YI)::value;
+                            constexpr col::CRect qr = col::rect(KIND, B, r);
+                            if constexpr (YLO + j >= qr.y0 && YLO + j < qr.y1) t0[(YLO + j - qr.y0) * w] = v[q][j];
+                        });
+                    }
+                } else {
+                    if (!dead && YLO + m >= q0.y0 && YLO + m < q0.y1) {
+                        double* t0 = tile + (YLO + m - q0.y0) * w;
+                        sfor<B>([&](auto XI) {
+                            constexpr int x = decltype(XI)::value;
+                            constexpr col::CRect qr = col::rect(KIND, B, r);
+                            if constexpr (x >= qr.x0 && x < qr.x1) t0[x - qr.x0] = v[q][x];
+                        });
+                    }
+                }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) {
+                const int m = CPL * l + q;
+                if constexpr (MODE == col::COL) {  // now ROW: m = window row
+                    if (YLO + m >= q0.y0 && YLO + m < q0.y1) {
+                        const double* t0 = tile + (YLO + m - q0.y0) * w;
+                        sfor<B>([&](auto XI) {
+                            constexpr int x = decltype(XI)::value;
+                            constexpr col::CRect qr = col::rect(KIND, B, r);
+                            if constexpr (x >= qr.x0 && x < qr.x1) v[q][x] = t0[x - qr.x0];
+                        });
+                    }
+                } else {  // now COL: m = column
+                    if (m >= q0.x0 && m < q0.x1) {
+                        const double* t0 = tile + (m - q0.x0);
+                        sfor<B>([&](auto YI) {
+                            constexpr int j = decltype(YI)::value;
+                            constexpr col::CRect qr = col::rect(KIND, B, r);
+                            if constexpr (YLO + j >= qr.y0 && YLO + j < qr.y1) v[q][j] = t0[(YLO + j - qr.y0) * w];
+                        });
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    });
+
+    // ---- partition-edge instances: copy the record into the neighbours' ghost rings
+    const bool edge = bi < gh || bi >= A.pbx - gh || bj < gh || bj >= A.pby - gh;
+    if (edge && live && A.nexp > 0) {
+        asm volatile("" ::: "memory");
+        if constexpr (L == 32) __syncwarp();
+        else __syncwarp(((1u << L) - 1u) << (sub * L));
+        for (int e = l; e < A.nexp; e += L) {
+            const double val = __ldcg(dst + e);
+            for (int ej = -1; ej <= 1; ++ej)
+                for (int ei = -1; ei <= 1; ++ei) {
+                    if (ei == 0 && ej == 0) continue;
+                    const int tbi = bi - ei * A.pbx, tbj = bj - ej * A.pby;
+                    if (tbi < -gh || tbi >= A.pbx + gh || tbj < -gh || tbj >= A.pby + gh) continue;
+                    const int tp = wrapi(pj + ej, A.py) * A.px + wrapi(pi + ei, A.px);
+                    A.rec[tp * A.nslots + A.my_slot][((long)(tbj + gh) * A.extw + (tbi + gh)) * A.epad + e] = val;
+                }
+        }
+    }
+}
+
+template <int B, int CPL, int WPC>
+cudaError_t launch_heat_col_t(const SweptArgs& a, cudaStream_t s) {
+    constexpr int IPC = WPC * (32 / (B / CPL));  // instances per CTA
+    const int ninst = a.pbx * a.pby;
+    const bool stash = (a.out_mask | a.snap_mask) != 0ull;
+    const size_t smem = static_cast<size_t>(IPC) * (a.smem_doubles + (stash ? B * B : 0)) * sizeof(double);
+    dim3 grid((ninst + IPC - 1) / IPC, a.ndev_parts);
+    auto go = [&](auto kern) {
+        if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<grid, WPC * 32, smem, s>>>(a);
+        return cudaGetLastError();
+    };
+    switch (a.kind) {
+        case col::UP: return go(swept_heat_col_kernel<B, col::UP, CPL, WPC>);
+        case col::YB: return go(swept_heat_col_kernel<B, col::YB, CPL, WPC>);
+        case col::XB: return go(swept_heat_col_kernel<B, col::XB, CPL, WPC>);
+        case col::OCT: return go(swept_heat_col_kernel<B, col::OCT, CPL, WPC>);
+        default: return go(swept_heat_col_kernel<B, col::DOWN, CPL, WPC>);
+    }
+}
+// One column (row) per lane: two per lane halves the shuffles but doubles the
+// live registers (Oct b16: 182 vs 106), and the lost occupancy costs more
+// (Oct launch 0.82 vs 0.62 ms, profiles/r01_summary.md).
+template <int B>
+cudaError_t launch_heat_col(const SweptArgs& a, cudaStream_t s) {
+    // 4 warps per CTA on big grids; single-warp CTAs when there are too few
+    // instances to fill the 148 SMs otherwise (the paper's 320^2..1120^2 grids)
+    if constexpr (B == 16)
+        if (a.pbx * a.pby * a.ndev_parts < 2 * 4 * 148 * 8) return launch_heat_col_t<B, 1, 1>(a, s);
+    // b16: 2-warp CTAs (finer-grained residency: 18 instead of 16 warps per
+    // SM at ~100 registers; 3.69e11 vs 3.65e11 (4 warps) and 3.61e11 (8))
+    if constexpr (B == 16) return launch_heat_col_t<B, 1, 2>(a, s);
+    return launch_heat_col_t<B, 1, 4>(a, s);
+}
+
+}  // namespace
+}  // namespace sg

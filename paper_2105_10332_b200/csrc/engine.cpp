@@ -136,9 +136,17 @@ Solver::Solver(const sg_config& cfg, int rank, int world) : cfg_(cfg), rank_(ran
         actual_steps_ = flat / eq.substeps;
         total_levels_ = flat;
         final_level_ = actual_steps_ * eq.substeps;  // engine.cpp:518
-        plan_ = compile_swept_plan(cfg_.block, eq, m, final_level_,
-                                   static_cast<long>(setup_.nx / cfg_.block) * (setup_.ny / cfg_.block),
-                                   static_cast<long>(pw_ / cfg_.block + 2) * (ph_ / cfg_.block + 2));
+        const long instances = static_cast<long>(setup_.nx / cfg_.block) * (setup_.ny / cfg_.block);
+        plan_ = compile_swept_plan(cfg_.block, eq, m, final_level_, instances);
+        if (plan_.colB) {
+            // the column kernels address every producer record as a 32-bit
+            // offset from the consumer's slot-0 record (imp_off): a partition's
+            // whole record ring -- its real slot count, ghost ring and record
+            // stride -- must fit, else the generic table-driven kernels run
+            const long ring = static_cast<long>(pw_ / cfg_.block + 2 * plan_.ghost) *
+                              (ph_ / cfg_.block + 2 * plan_.ghost) * plan_.max_epad * plan_.nslots;
+            if (ring >= 0x7fffffffL) plan_ = compile_swept_plan(cfg_.block, eq, m, final_level_, 1);
+        }
         for (const Launch& l : plan_.launches)
             cell_updates_ += static_cast<long long>(plan_.updates_per_kind[l.kind]) *
                              (setup_.nx / cfg_.block) * (setup_.ny / cfg_.block);

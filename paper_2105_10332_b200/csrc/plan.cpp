@@ -138,12 +138,11 @@ SweptPlan compile_swept_plan(int b, const Equation& eq, long m, long final_level
     {
         const char* env = std::getenv("SG_HEAT_KERNEL");
         const bool forced = env && std::strcmp(env, "column") == 0;
-        bool generic = (env && std::strcmp(env, "generic") == 0) || (!forced && instances > 0 && instances < 2048);
-        if (eq.problem == SG_HEAT && col::supported(b)) {
-            long epad = 0;  // the column record stride (plan: K.epad = exported cells rounded to 4)
-            for (int kd = 0; kd < K_NKINDS; ++kd) epad = std::max<long>(epad, (col::exp_total(kd, b) + 3) / 4 * 4);
-            if (partition_instances * epad * 7 >= 0x7fffffffL) generic = true;  // 7 = record slots
-        }
+        // (a record ring too large for the column kernels' 32-bit gather
+        // offsets is caught by the engine, which then recompiles generic)
+        (void)partition_instances;
+        const bool generic =
+            (env && std::strcmp(env, "generic") == 0) || (!forced && instances > 0 && instances < 2048);
         if (eq.problem == SG_HEAT && n == 1 && S == 1 && col::supported(b) && !generic) P.colB = b;
     }
     if (final_level < 1 || final_level > P.flat) fail(SG_ELOGIC, "plan: final level outside the schedule");

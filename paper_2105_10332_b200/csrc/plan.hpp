@@ -125,12 +125,12 @@ void spread_banks(std::vector<T>& v, std::size_t begin, std::size_t end, Key key
 
 // m = octahedra; final_level = the level the run must output; instances =
 // block instances per launch over all partitions (0: unknown).  Heat runs with
-// b in {8, 16, 32} use the register-tile kernels (colgeom.hpp) unless
+// b in {8, 12, 16, 24, 32} use the register-tile kernels (colgeom.hpp) unless
 // SG_HEAT_KERNEL=generic is set, or the grid is so small (< 2048 instances)
 // that the per-instance latency of the generic kernels wins (SG_HEAT_KERNEL=
-// column forces them), or a partition so large that the record ring of one
-// partition (7 slots) would exceed the kernels' 32-bit gather offsets
-// (partition_instances = (pw/b + 2) * (ph/b + 2), ghost ring included).
+// column forces them).  (The engine recompiles with instances = 1, i.e.
+// generic, when a partition's record ring would exceed the column kernels'
+// 32-bit gather offsets; partition_instances is unused.)
 SweptPlan compile_swept_plan(int b, const Equation& eq, long m, long final_level, long instances = 0,
                              long partition_instances = 0);
 
