@@ -385,6 +385,147 @@ __global__ void __launch_bounds__(256, MINB) std_euler_kernel(const __grid_const
     if (err) *A.err = 1;
 }
 
+// Standard Euler step, column marching (no shared memory, no barriers): a
+// warp owns 31 consecutive columns (lane L = column x0 - 1 + L) of a strip of
+// ROWS rows and walks down it.  Per row j:
+//   * y-interface j+1/2 (euler_row_fast's shared fluxes, physics.cpp:270-321):
+//     the lane keeps its column's rows j-1..j+2 (and their pressures) in a
+//     register window, one new row loaded per step; the flux of j-1/2 is the
+//     previous step's j+1/2;
+//   * x-interface x+1/2 from the cells x-1..x+2 of row j (the neighbours'
+//     cells come from L1; their pressures are recomputed -- cheaper than the
+//     divergent edge handling shuffles would need); the flux of x-1/2 is lane
+//     L-1's, by shuffle (lane 0 only supplies it);
+//   * out = base - cx*(fe - fw) - cy*(gn - gs) (physics.cpp:131-156), plus the
+//     pushes of partition-edge cells into the neighbours' ghost frames.
+// Non-physical states seen on a path an output cell needs raise the error flag.
+template <int ROWS>
+__global__ void __launch_bounds__(128, 4) std_euler_col_kernel(const __grid_constant__ StdArgs A) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int x0 = (blockIdx.x * 4 + warp) * 31;
+    const int x = x0 - 1 + lane;
+    if (x0 >= A.pw) return;  // whole warp past the partition
+    const bool active = x < A.pw;         // computes a needed x-flux
+    const bool outl = active && lane > 0;  // owns an output cell
+    const int xc = active ? x : A.pw - 1;  // loads stay inside the ghosted plane
+    const int ybeg = blockIdx.y * ROWS, yend = min(ybeg + ROWS, A.ph);
+    const int part = A.dev_parts[blockIdx.z];
+    const int P = A.pitch;
+    const long pl = (long)A.pitch * A.rows;
+    const double* r1 = A.read1[part];
+    const double* bse = A.stage == 1 ? A.read2[part] : r1;
+    double* out = A.out[part];
+    const int pi = part % A.px, pj = part / A.px;
+    const double gamma = A.c0, cx = A.c1, cy = A.c2;
+    auto at = [&](int xx, int yy) { return (long)(yy + 2) * P + (xx + 2); };
+    int errx = 0, erry = 0;
+    // window: rows j-1, j, j+1, j+2 of column xc (w[0..3]) and their pressures
+    double w[4][4], pw_[4], gs[4];
+    auto load = [&](int yy, double q[4]) {
+        const double* g = r1 + at(xc, yy);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) q[v] = __ldg(g + v * pl);
+    };
+    // prologue: rows ybeg-2 .. ybeg+1 -> flux of ybeg-1/2
+    {
+        double t[4][4], tp[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            load(ybeg - 2 + k, t[k]);
+            tp[k] = pressure_d(t[k], gamma, erry);
+        }
+        iface_flux_d<1>(t, tp, gamma, gs, erry);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) w[k][v] = t[k + 1][v];
+            pw_[k] = tp[k + 1];
+        }
+    }
+    // (issuing the next row's loads one step ahead was measured: +4 % at
+    // 4096^2, -15 % at 960^2 from the lost occupancy at 162 registers; a 5th
+    // or 6th resident CTA needs spills and is slower)
+    auto load_x = [&](int yy, double q[3][4]) {
+        const double* g = r1 + at(xc, yy);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            q[0][v] = __ldg(g - 1 + v * pl);
+            q[1][v] = __ldg(g + 1 + v * pl);
+            q[2][v] = __ldg(g + 2 + v * pl);
+        }
+    };
+    for (int y = ybeg; y < yend; ++y) {
+        // new row y+2 enters the window (rows y-1 .. y+2); x-stencil of row y
+        double xs[3][4];
+        load(y + 2, w[3]);
+        load_x(y, xs);
+        pw_[3] = pressure_d(w[3], gamma, erry);
+        double gn[4];
+        iface_flux_d<1>(w, pw_, gamma, gn, erry);
+        // x-interface x+1/2 of row y: cells x-1, x, x+1, x+2
+        double fe[4];
+        {
+            double q[4][4], p[4];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                q[0][v] = xs[0][v];
+                q[1][v] = w[1][v];
+                q[2][v] = xs[1][v];
+                q[3][v] = xs[2][v];
+            }
+            p[0] = pressure_d(q[0], gamma, errx);
+            p[1] = pw_[1];
+            p[2] = pressure_d(q[2], gamma, errx);
+            p[3] = pressure_d(q[3], gamma, errx);
+            iface_flux_d<0>(q, p, gamma, fe, errx);
+        }
+        double o[4];
+        const long idx = at(xc, y);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const double fw = __shfl_up_sync(0xffffffffu, fe[v], 1);
+            o[v] = __ldg(bse + idx + v * pl) - cx * (fe[v] - fw) - cy * (gn[v] - gs[v]);
+        }
+        if (outl) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) out[idx + v * pl] = o[v];
+            // partition-edge cells -> the neighbours' ghost frames (cross stencil: no corners)
+            if (x < 2) {
+                double* g = A.out[pj * A.px + (pi + A.px - 1) % A.px] + at(x + A.pw, y);
+#pragma unroll
+                for (int v = 0; v < 4; ++v) g[v * pl] = o[v];
+            }
+            if (x >= A.pw - 2) {
+                double* g = A.out[pj * A.px + (pi + 1) % A.px] + at(x - A.pw, y);
+#pragma unroll
+                for (int v = 0; v < 4; ++v) g[v * pl] = o[v];
+            }
+            if (y < 2) {
+                double* g = A.out[((pj + A.py - 1) % A.py) * A.px + pi] + at(x, y + A.ph);
+#pragma unroll
+                for (int v = 0; v < 4; ++v) g[v * pl] = o[v];
+            }
+            if (y >= A.ph - 2) {
+                double* g = A.out[((pj + 1) % A.py) * A.px + pi] + at(x, y - A.ph);
+#pragma unroll
+                for (int v = 0; v < 4; ++v) g[v * pl] = o[v];
+            }
+        }
+        // slide
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            gs[v] = gn[v];
+            w[0][v] = w[1][v];
+            w[1][v] = w[2][v];
+            w[2][v] = w[3][v];
+        }
+        pw_[0] = pw_[1];
+        pw_[1] = pw_[2];
+        pw_[2] = pw_[3];
+    }
+    if ((active && errx) || (outl && erry)) *A.err = 1;
+}
+
 // Standard heat step, column marching: a thread owns two adjacent columns of
 // a 256 x ROWS tile and walks down them four rows per trip with 16-byte
 // loads/stores; centre/south stay in registers and the E/W neighbours of the
@@ -656,6 +797,22 @@ cudaError_t launch_std(int problem, const StdArgs& a, cudaStream_t s) {
         dim3 grid((a.pw / 2 + 127) / 128, (a.ph + ROWS - 1) / ROWS, a.ndev_parts);
         std_heat_kernel<ROWS><<<grid, 128, 0, s>>>(a);
         return cudaGetLastError();
+    }
+    if (problem == 1 && !std::getenv("SG_EULER_TILE")) {
+        // column marching: 124 columns x ROWS rows per 4-warp CTA; ROWS as
+        // large as keeps ~16 warps per SM busy (each strip re-reads 3 rows)
+        const long warps = (a.pw + 123) / 124 * 4L * a.ndev_parts;
+        const long want_rows = a.ph * warps / (148L * 16);
+        dim3 grid((a.pw + 123) / 124, 1, a.ndev_parts);
+        auto go = [&](auto kern, int rows) {
+            grid.y = (a.ph + rows - 1) / rows;
+            kern<<<grid, 128, 0, s>>>(a);
+            return cudaGetLastError();
+        };
+        if (want_rows >= 64) return go(std_euler_col_kernel<64>, 64);
+        if (want_rows >= 32) return go(std_euler_col_kernel<32>, 32);
+        if (want_rows >= 16) return go(std_euler_col_kernel<16>, 16);
+        return go(std_euler_col_kernel<8>, 8);
     }
     if (problem == 1) {
         // 32 x 7: the fused flux step has 7*33 + 8*32 = 487 items = two rounds of 256
