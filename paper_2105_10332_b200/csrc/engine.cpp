@@ -199,10 +199,8 @@ void Solver::build_swept() {
     // one instance's phase must fit on chip (levels + Euler flux scratch)
     int inst_smem = 0;
     for (int kd = 0; kd < K_NKINDS; ++kd) inst_smem = std::max(inst_smem, P.kinds[kd].smem_doubles * 8);
-    if (inst_smem > 160 * 1024)
+    if (inst_smem > 220 * 1024)
         fail(SG_EINVAL, "swept: block too large for the on-chip phases (shared memory per instance)");
-    if (setup_.eq.problem == SG_HEAT && b != 8 && b != 12 && b != 16 && b != 24 && b != 32)
-        fail(SG_EINVAL, "swept heat: block must be one of 8, 12, 16, 24, 32 on the GPU");
 
     if (!snap_path_.empty()) {
         // level l is complete after the last launch computing it; frames are
@@ -459,8 +457,6 @@ void Solver::finalize_swept() {
                 hl.cbw = Lc.pitch;
                 hl.inv_w = w > 0 ? 1.0f / static_cast<float>(w) : 0.0f;
                 hl.pad = 0;
-                if (setup_.eq.problem == SG_HEAT && w > 32)
-                    fail(SG_EINVAL, "swept heat: phase rectangle wider than a warp (block > 34)");
                 a.hl[r - 1] = hl;
             }
             d.swept_args.push_back(a);

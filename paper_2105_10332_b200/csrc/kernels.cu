@@ -139,15 +139,8 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_kernel(const __grid_const
     for (int r = 1; r <= A.nlev; ++r) {
         const HeatLevel& L = A.hl[r - 1];
         const int bp = L.pbw, bc = L.cbw;
-        int x = 0, y0 = 0, n = 0;
-        if (lane < L.items) {
-            // item -> (column, row chunk); exact (items < 2^5, w <= 2^5)
-            const int ch = __float2int_rz((lane + 0.5f) * L.inv_w);
-            x = L.cx0 + (lane - ch * L.w);
-            y0 = L.cy0 + ch * L.rps;
-            n = min(L.rps, L.cy1 - y0);
-        }
-        if (n > 0) {
+        // rows [y0, y0 + n) of column x: walk down, four rows per trip
+        auto walk = [&](int x, int y0, int n) {
             const double* P = S + L.poff + y0 * bp + x;
             double* D = S + L.doff + y0 * bc + x;
             double south = P[-bp], c = P[0];
@@ -194,6 +187,19 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_kernel(const __grid_const
                     if (snap) A.frames[opj * A.px + opi][(lev % A.frame_ring) * pl + o] = *Dv;
                 }
             }
+        };
+        if (L.items > 0) {
+            if (lane < L.items) {
+                // item -> (column, row chunk); exact (items < 2^5, w <= 2^5)
+                const int ch = __float2int_rz((lane + 0.5f) * L.inv_w);
+                const int x = L.cx0 + (lane - ch * L.w);
+                const int y0 = L.cy0 + ch * L.rps;
+                const int n = min(L.rps, L.cy1 - y0);
+                if (n > 0) walk(x, y0, n);
+            }
+        } else {
+            // rectangles wider than a warp (block > 34): lanes stride the columns
+            for (int x = L.cx0 + lane; x < L.cx0 + L.w; x += 32) walk(x, L.cy0, L.cy1 - L.cy0);
         }
         __syncwarp();
         if (r == A.split && A.nexp_early > 0) {

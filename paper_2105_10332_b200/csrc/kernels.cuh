@@ -5,7 +5,7 @@
 
 namespace sg {
 
-constexpr int kMaxLevels = 40;   // relative levels per kind (2k + 2 <= 40 -> b <= 36 heat)
+constexpr int kMaxLevels = 64;   // relative levels per kind (2k + 2 <= 64; level masks are 64-bit)
 constexpr int kMaxSegs = 24;
 constexpr int kMaxParts = 64;
 
