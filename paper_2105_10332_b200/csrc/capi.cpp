@@ -100,8 +100,6 @@ int sg_solver_create(const sg_config* cfg, sg_solver** out, char* err, size_t er
 int sg_dist_create(const sg_config* cfg, int rank, int world, sg_solver** out, char* err, size_t errlen) {
     *out = nullptr;
     return guard(err, errlen, [&] {
-        if (cfg->snapshot_path && cfg->snapshot_path[0])
-            sg::fail(SG_EINVAL, "snapshots are not supported by the distributed solver");
         auto* h = new sg_solver{nullptr};
         try {
             h->s = new sg::Solver(*cfg, rank, world);

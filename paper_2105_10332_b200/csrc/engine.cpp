@@ -41,7 +41,6 @@ Solver::Solver(const sg_config& cfg, int rank, int world) : cfg_(cfg), rank_(ran
     const auto t0 = std::chrono::steady_clock::now();
     setup_ = make_setup(cfg_);
     if (cfg_.snapshot_path && cfg_.snapshot_path[0]) {
-        if (dist()) fail(SG_EINVAL, "snapshots are not supported by the distributed solver");
         snap_path_ = cfg_.snapshot_path;
         snap_every_ = cfg_.snapshot_every;
     }
@@ -170,6 +169,16 @@ Solver::Solver(const sg_config& cfg, int rank, int world) : cfg_(cfg), rank_(ran
 
 Solver::~Solver() {
     if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+    for (double* h : drain_.host) cudaFreeHost(h);
+    for (auto& d : devs_) {
+        cudaSetDevice(d.dev);
+        if (d.copy) {
+            cudaStreamSynchronize(d.copy);
+            cudaStreamDestroy(d.copy);
+        }
+        if (d.ev_ready) cudaEventDestroy(d.ev_ready);
+        for (auto e : d.ev_copied) cudaEventDestroy(e);
+    }
     for (auto& d : devs_) {
         cudaSetDevice(d.dev);
         cudaStreamSynchronize(d.stream);
@@ -218,7 +227,9 @@ void Solver::build_swept() {
             width = std::max(width, highest - lowest + 1);
             for (long l : done_after_[i]) lowest = std::max(lowest, l + 1);
         }
-        frame_ring_ = static_cast<int>(width);
+        // + spare slots: a completed frame's D2H (copy stream) overlaps the
+        // next launches instead of blocking the first one that reuses its slot
+        frame_ring_ = static_cast<int>(width) + (dist() ? 0 : 2);
     }
     for (auto& pb : parts_) {
         if (pb.dev < 0) continue;
@@ -601,7 +612,8 @@ double Solver::solve() {
     }
     if (dist()) dist_barrier(devs_[0]);  // no rank starts writing into a peer still in its previous solve
     std::unique_ptr<SnapshotWriter> writer;
-    if (!snap_path_.empty()) {  // FrameSink, engine.cpp:75-117 of the reference
+    const bool snap = !snap_path_.empty();
+    if (snap && (!dist() || rank_ == 0)) {  // FrameSink, engine.cpp:75-117 of the reference
         SnapshotMeta m;
         m.problem = setup_.eq.problem == SG_HEAT ? "heat" : "euler";
         m.nx = setup_.nx;
@@ -623,7 +635,7 @@ double Solver::solve() {
     // Cross-stream edges come from the plan: producer launches (segments),
     // earlier readers of the record slot a launch overwrites, and its previous
     // writer.
-    const bool concurrent = cfg_.engine == SG_SWEPT && !multi && !dist() && !writer && !profile &&
+    const bool concurrent = cfg_.engine == SG_SWEPT && !multi && !dist() && !snap && !profile &&
                             !std::getenv("SG_SERIAL_BRIDGES");
     std::vector<int> on_side;
     if (concurrent) {
@@ -648,6 +660,27 @@ double Solver::solve() {
                     if (q - sg.delta == L - n) deps.push_back(q);
         }
         return deps;
+    };
+    // snapshot levels: one process -> overlapped drain (D2H on the copy
+    // streams, launches that reuse a frame slot wait for its copy); one
+    // process per GPU -> rank 0 gathers every partition's frame through the
+    // IPC-mapped buffers after the launch barrier, then all ranks pass one
+    // more barrier so no peer overwrites a frame slot still being read
+    auto snap_before = [&](long lo, long hi, int ring) {
+        if (!snap || dist()) return;
+        for (long l = lo; l <= hi; ++l)
+            if (l % snap_every_ == 0) drain_wait_slot(static_cast<int>(l % ring));
+    };
+    auto snap_after = [&](const std::vector<long>& done, int ring) {
+        if (!snap) return;
+        bool any = false;
+        for (long l : done)
+            if (l % snap_every_ == 0) {
+                any = true;
+                if (!dist()) drain_start(*writer, l, static_cast<int>(l % ring));
+                else if (writer) snapshot_frame(*writer, l, static_cast<int>(l % ring));
+            }
+        if (any && dist()) dist_barrier(devs_[0]);
     };
     auto enqueue = [&]() {
         if (cfg_.engine == SG_SWEPT) {
@@ -675,6 +708,7 @@ double Solver::solve() {
                     if (side) last_side = static_cast<long>(li);
                     continue;
                 }
+                snap_before(plan_.launches[li].lo, plan_.launches[li].hi, frame_ring_);
                 for (auto& d : devs_) {
                     if (multi) cudaSetDevice(d.dev);
                     if (&d == &d0) prof_begin(pr);
@@ -693,9 +727,7 @@ double Solver::solve() {
                     prof_updates_ += inst * plan_.updates_per_kind[L.kind];
                 }
                 cross_sync();
-                if (writer)
-                    for (long l : done_after_[li])
-                        if (l % snap_every_ == 0) snapshot_frame(*writer, l, static_cast<int>(l % frame_ring_));
+                if (snap) snap_after(done_after_[li], frame_ring_);
             }
             if (concurrent) {  // join: the main stream waits for the side stream's last launch
                 if (last_side >= 0) ck(cudaStreamWaitEvent(d0.stream, d0.launch_ev[last_side], 0), "wait");
@@ -711,6 +743,7 @@ double Solver::solve() {
                 const int phase = static_cast<int>(l % (S + 1));
                 const int stage = static_cast<int>((l - 1) % S);
                 const bool pr = profile;
+                snap_before(l, l, S + 1);
                 for (auto& d : devs_) {
                     if (multi) cudaSetDevice(d.dev);
                     StdArgs a;
@@ -752,14 +785,14 @@ double Solver::solve() {
                     prof_updates_ += cells;
                 }
                 cross_sync();
-                if (writer && l % snap_every_ == 0) snapshot_frame(*writer, l, static_cast<int>(l % (S + 1)));
+                if (snap) snap_after({l}, S + 1);
             }
         }
     };
     // Single-GPU solves without snapshots/profiling are replayed from a CUDA
     // graph captured on the first solve: every launch of the solve (up to
     // ~4300 phase launches at 10k steps) goes to the GPU in one call.
-    const bool graphable = !multi && !dist() && !writer && !profile && use_graph_;
+    const bool graphable = !multi && !dist() && !snap && !profile && use_graph_;
     if (graphable) {
         DeviceCtx& d = devs_[0];
         if (!graph_exec_) {
@@ -795,6 +828,7 @@ double Solver::solve() {
     }
     last_solve_ = worst;
     if (writer) {
+        while (!drain_.queue.empty()) drain_pop(*writer);
         writer->flush();
         snapshot_frames_ = writer->frames();
     }
@@ -810,8 +844,8 @@ void Solver::snapshot_frame(SnapshotWriter& w, long level, int slot) {
     const std::size_t nx = setup_.nx, ny = setup_.ny, plane = static_cast<std::size_t>(pw_) * ph_;
     std::vector<double> full(nv * nx * ny), piece;
     for (auto& pb : parts_) {
-        if (pb.dev < 0) continue;
-        DeviceCtx& d = devs_[pb.dev];
+        if (pb.dev < 0 && !dist()) continue;
+        DeviceCtx& d = devs_[pb.dev < 0 ? 0 : pb.dev];  // remote partitions: IPC-mapped buffers
         cudaSetDevice(d.dev);
         ck(cudaStreamSynchronize(d.stream), "snapshot sync");
         if (cfg_.engine == SG_SWEPT) {
@@ -835,6 +869,88 @@ void Solver::snapshot_frame(SnapshotWriter& w, long level, int slot) {
         }
     }
     w.append_frame(level, full.data());
+}
+
+int Solver::nslots_frames() const {
+    return cfg_.engine == SG_SWEPT ? frame_ring_ : setup_.eq.substeps + 1;
+}
+
+void Solver::drain_start(SnapshotWriter& w, long level, int slot) {
+    FrameDrain& D = drain_;
+    const Equation& eq = setup_.eq;
+    const int nv = eq.nvars;
+    const std::size_t nx = setup_.nx, ny = setup_.ny, plane = static_cast<std::size_t>(pw_) * ph_;
+    if (D.host.empty()) {
+        const std::size_t bytes = sizeof(double) * nv * nx * ny;
+        const int K = bytes <= (512ull << 20) ? 3 : bytes <= (2048ull << 20) ? 2 : 1;
+        D.host.assign(K, nullptr);
+        for (auto& h : D.host) ck(cudaMallocHost(&h, bytes), "cudaMallocHost");
+        D.level.assign(K, -1);
+        D.slot_host.assign(nslots_frames(), -1);
+        for (auto& d : devs_) {
+            ck(cudaSetDevice(d.dev), "cudaSetDevice");
+            ck(cudaStreamCreateWithFlags(&d.copy, cudaStreamNonBlocking), "stream");
+            ck(cudaEventCreateWithFlags(&d.ev_ready, cudaEventDisableTiming), "event");
+            d.ev_copied.resize(K);
+            for (auto& e : d.ev_copied) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        }
+    }
+    const int k = D.next;
+    D.next = (k + 1) % static_cast<int>(D.host.size());
+    while (D.level[k] >= 0) drain_pop(w);  // round robin: frame k is the oldest pending
+    double* host = D.host[k];
+    for (auto& d : devs_) {
+        ck(cudaSetDevice(d.dev), "cudaSetDevice");
+        ck(cudaEventRecord(d.ev_ready, d.stream), "event");
+        ck(cudaStreamWaitEvent(d.copy, d.ev_ready, 0), "wait");
+        for (int p : d.parts) {
+            const PartBuffers& pb = parts_[p];
+            for (int v = 0; v < nv; ++v) {
+                double* dst = host + (static_cast<std::size_t>(v) * ny + static_cast<std::size_t>(pb.pj) * ph_) * nx +
+                              static_cast<std::size_t>(pb.pi) * pw_;
+                if (cfg_.engine == SG_SWEPT) {
+                    const double* src = pb.frames + (static_cast<std::size_t>(slot) * nv + v) * plane;
+                    ck(cudaMemcpy2DAsync(dst, nx * sizeof(double), src, pw_ * sizeof(double), pw_ * sizeof(double),
+                                         ph_, cudaMemcpyDeviceToHost, d.copy),
+                       "snapshot D2H");
+                } else {
+                    const int n = eq.halo, pitch = pw_ + 2 * n, rows = ph_ + 2 * n;
+                    const double* src = pb.ring[slot] + static_cast<std::size_t>(v) * pitch * rows +
+                                        static_cast<std::size_t>(n) * pitch + n;
+                    ck(cudaMemcpy2DAsync(dst, nx * sizeof(double), src, pitch * sizeof(double), pw_ * sizeof(double),
+                                         ph_, cudaMemcpyDeviceToHost, d.copy),
+                       "snapshot D2H");
+                }
+            }
+        }
+        ck(cudaEventRecord(d.ev_copied[k], d.copy), "event");
+    }
+    D.level[k] = level;
+    D.slot_host[slot] = k;
+    D.queue.push_back({level, k});
+}
+
+void Solver::drain_wait_slot(int slot) {
+    FrameDrain& D = drain_;
+    if (D.slot_host.empty() || D.slot_host[slot] < 0) return;
+    const int k = D.slot_host[slot];
+    for (auto& d : devs_) {
+        cudaSetDevice(d.dev);
+        for (auto& e : devs_) ck(cudaStreamWaitEvent(d.stream, e.ev_copied[k], 0), "wait");
+    }
+    D.slot_host[slot] = -1;
+}
+
+void Solver::drain_pop(SnapshotWriter& w) {
+    FrameDrain& D = drain_;
+    const auto [level, k] = D.queue.front();
+    for (auto& d : devs_) {
+        cudaSetDevice(d.dev);
+        ck(cudaEventSynchronize(d.ev_copied[k]), "snapshot D2H");
+    }
+    w.append_frame(level, D.host[k]);
+    D.level[k] = -1;
+    D.queue.erase(D.queue.begin());
 }
 
 void Solver::check_error() {
@@ -866,6 +982,7 @@ std::vector<unsigned char> Solver::ipc_blob() const {
         bufs.push_back(pb.rec[0]);  // all slots: one allocation
         bufs.push_back(pb.init);
         bufs.push_back(pb.out);
+        if (pb.frames) bufs.push_back(pb.frames);  // snapshot frame ring (peers write edge cells)
     } else {
         for (double* r : pb.ring) bufs.push_back(r);
         bufs.push_back(pb.init_ghosted);
@@ -904,6 +1021,7 @@ void Solver::connect(const unsigned char* blobs, std::size_t per_rank) {
             for (int s2 = 0; s2 < plan_.nslots; ++s2) pb.rec[s2] = all + rec_len_ * s2;
             pb.init = static_cast<double*>(p[i++]);
             pb.out = static_cast<double*>(p[i++]);
+            if (frame_ring_ > 0) pb.frames = static_cast<double*>(p[i++]);
         } else {
             pb.ring.resize(setup_.eq.substeps + 1);
             for (auto& r : pb.ring) r = static_cast<double*>(p[i++]);

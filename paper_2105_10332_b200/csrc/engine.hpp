@@ -59,6 +59,21 @@ struct DeviceCtx {
     // concurrent bridges (single device): a second stream and one event per launch
     cudaStream_t side = nullptr;
     std::vector<cudaEvent_t> launch_ev;
+    // snapshot drain: D2H copies of completed frames on their own stream
+    cudaStream_t copy = nullptr;
+    cudaEvent_t ev_ready = nullptr;            // compute stream: frame level complete
+    std::vector<cudaEvent_t> ev_copied;        // per pinned host frame: copies done
+};
+
+// Snapshot frames in flight (one process): pinned host frames filled by
+// cudaMemcpy2DAsync on each device's copy stream while the solve goes on;
+// written to the SWPT2D file in level order once their copies completed.
+struct FrameDrain {
+    std::vector<double*> host;                 // pinned full frames [var][ny][nx]
+    std::vector<long> level;                   // level held by host frame k (-1: free)
+    std::vector<int> slot_host;                // device frame slot -> host frame copying it (-1: none)
+    std::vector<std::pair<long, int>> queue;   // (level, host frame) in append order
+    int next = 0;
 };
 
 class Solver {
@@ -124,6 +139,13 @@ class Solver {
     std::vector<std::vector<long>> done_after_;  // swept: levels completed by launch i
     long snapshot_frames_ = 0;
     void snapshot_frame(SnapshotWriter& w, long level, int slot_or_ring);  // D2H + assemble + append
+    // one process: start the D2H of level `level` (device frame `slot`) after
+    // the work enqueued so far; wait for host frames / device slots as needed
+    void drain_start(SnapshotWriter& w, long level, int slot);
+    void drain_wait_slot(int slot);            // compute streams wait until `slot` was copied out
+    void drain_pop(SnapshotWriter& w);         // oldest pending frame -> file
+    FrameDrain drain_;
+    int nslots_frames() const;
     // profiling of the dominant kernel class
     int prof_kind_ = -1;
     double prof_seconds_ = 0.0;
