@@ -116,3 +116,31 @@ def test_fnv1a64_matches_reference_convention(sg, oracle):
     import numpy as np
     a = np.arange(1000, dtype=np.float64) * 0.37
     assert sg.fnv1a64(a) == oracle.fnv1a(a)
+
+
+def test_reference_shim_compiles(tmp_path):
+    """include/sweptgrid_gpu.hpp (the reference-side binding, INTEGRATION.md
+    section 1) compiles against the reference's own headers and links against
+    libsweptgpu.so; run_gpu has sweptgrid::run's signature."""
+    import shutil
+    import subprocess
+    ref_inc = Path("/root/reference/proj/include")
+    if not ref_inc.is_dir():
+        pytest.skip("reference headers not present (GPU box)")
+    json_dir = Path("/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann")
+    cxx = shutil.which("g++")
+    if not cxx or not json_dir.is_dir():
+        pytest.skip("g++ or nlohmann/json missing")
+    src = tmp_path / "shim.cpp"
+    src.write_text('#include "sweptgrid_gpu.hpp"\n'
+                   'sweptgrid::RunResult (*fp)(const sweptgrid::SolverConfig&) = &sweptgrid::run_gpu;\n'
+                   'int main() { return fp == nullptr; }\n')
+    lib = ROOT / "paper_2105_10332_b200"
+    # the shim uses only header-inline reference code plus problem_name,
+    # NonPhysicalState and FieldState from the reference library: link it too
+    ref_lib = ROOT / "oracle" / "_ref"
+    cmd = [cxx, "-std=gnu++20", "-O0", f"-I{ROOT / 'include'}", f"-I{ref_inc}", f"-I{json_dir}", str(src),
+           "-o", str(tmp_path / "shim"), f"-L{lib}", "-lsweptgpu", f"-L{ref_lib}", "-lsweptgrid_ref",
+           f"-Wl,-rpath,{lib}:{ref_lib}", "-fopenmp"]
+    p = subprocess.run(cmd, capture_output=True, text=True)
+    assert p.returncode == 0, p.stderr[-3000:]

@@ -72,3 +72,30 @@ def test_euler_8192_partitioned(sg, px, py):
 
 def test_euler_8192_standard_partitioned(sg):
     _check(sg, _case("euler", 8192, 16), "standard", ranks=4, px=2, py=2)
+
+
+@pytest.mark.parametrize("cfg", [
+    {"problem": "heat", "nx": 384, "block": 16, "steps": 500, "engine": "swept"},
+    {"problem": "heat", "nx": 96, "block": 8, "steps": 50, "engine": "standard", "ranks": 2},
+    {"problem": "euler", "nx": 96, "block": 16, "steps": 20, "engine": "swept", "ranks": 2},
+])
+def test_reference_side_dropin(sg, cfg):
+    """The reference's own SolverConfig/RunRecord code calling the GPU through
+    include/sweptgrid_gpu.hpp (oracle/_ref/shim_run) prints the same record
+    and final-field hash as the unmodified CPU reference (oracle/_ref/ref_run)."""
+    import subprocess
+    if sg.device_count() < 1:
+        pytest.fail("no CUDA device")
+    root = Path(__file__).resolve().parents[1]
+    shim, ref = root / "oracle" / "_ref" / "shim_run", root / "oracle" / "_ref" / "ref_run"
+    if not shim.exists() or not ref.exists():
+        pytest.skip("oracle/_ref not built (needs /root/reference at build time)")
+    a = json.loads(subprocess.run([str(shim), json.dumps(cfg)], capture_output=True, text=True,
+                                  timeout=300).stdout.strip().splitlines()[-1])
+    b = json.loads(subprocess.run([str(ref), json.dumps(cfg), "1"], capture_output=True, text=True,
+                                  timeout=300).stdout.strip().splitlines()[-1])
+    assert "error" not in a, a
+    for k in ("engine", "problem", "nx", "block", "ranks", "steps_requested", "actual_steps", "total_levels",
+              "octahedra", "communicates", "dt", "cell_updates", "final_level", "fnv1a64"):
+        assert a[k] == b[k], (k, a[k], b[k])
+    assert len(a["per_rank"]) == cfg.get("ranks", 1)
