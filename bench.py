@@ -110,7 +110,7 @@ def ncu_traffic(tag: str):
             j = json.loads(p.read_text())
         except Exception:  # noqa: BLE001
             continue
-        if j.get("workload") == tag and j.get("dram_bytes_per_launch"):
+        if isinstance(j, dict) and j.get("workload") == tag and j.get("dram_bytes_per_launch"):
             best = (j["dram_bytes_per_launch"], p.name)
     return best
 
@@ -419,6 +419,20 @@ def main():
                 s.close()
             eu["swept_over_standard"] = eu["swept"]["value"] / eu["standard"]["value"]
             extra["euler_960_b16"] = eu
+            # the same grid at b32 (the largest Euler block whose phase fits on chip)
+            s = sg.Solver(sg.SolverConfig(problem="euler", nx=960, block=32, engine="swept", steps=500))
+            for _ in range(3):
+                s.reset()
+                s.solve()
+            ts = []
+            for _ in range(args.steps):
+                s.reset()
+                ts.append(s.solve())
+            r32 = s.fetch().record
+            s.close()
+            extra["euler_960_b32_swept"] = {"value": r32.cell_updates * args.steps / sum(ts),
+                                            "actual_steps": r32.actual_steps,
+                                            "ms_per_step": 1e3 * sum(ts) / args.steps}
             # the paper's own array sizes, b16, 500 requested steps:
             # the launch/latency-bound regime the swept rule targets
             ps = {}

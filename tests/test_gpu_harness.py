@@ -55,3 +55,36 @@ def test_sweep_csv_schema(sg, tmp_path):
     assert len(rows) == 4 and all(r["error"] == "" and float(r["speedup"]) > 0 for r in rows)
     harness.run_sweep(spec, str(path))  # resume: nothing new
     assert len(harness.load_bench_csv(str(path))) == 4
+
+
+def test_weak_scaling_csv(sg, tmp_path):
+    """run_weak_scaling CSV (bench.cpp:208-244): the reference's rank ladder
+    (1, 192) .. (4, 384), block 16, share 0.9, standard then swept per rung;
+    points per rank, per-step seconds and bytes per exchange event derived
+    from the record exactly as the reference does."""
+    _gpu(sg)
+    import csv
+    from paper_2105_10332_b200 import harness
+    spec = harness.SweepSpec(problems=["heat", "euler"], array_sizes=[], block_sizes=[16], shares=[0.9], steps=20)
+    path = tmp_path / "weak.csv"
+    harness.run_weak_scaling(spec, str(path))
+    rows = list(csv.DictReader(open(path)))
+    assert list(rows[0]) == ["problem", "ranks", "nx", "points_per_rank", "engine", "actual_steps", "seconds",
+                             "seconds_per_step", "messages", "bytes", "bytes_per_event"]
+    assert len(rows) == 2 * 4 * 2
+    for r in rows:
+        ranks, nx = int(r["ranks"]), int(r["nx"])
+        assert (ranks, nx) in ((1, 192), (2, 288), (3, 336), (4, 384))
+        assert int(r["points_per_rank"]) == nx * nx // ranks
+        assert float(r["seconds"]) > 0
+        assert float(r["seconds_per_step"]) == pytest.approx(float(r["seconds"]) / int(r["actual_steps"]))
+        if ranks > 1:
+            assert int(r["messages"]) > 0 and int(r["bytes"]) > 0 and float(r["bytes_per_event"]) > 0
+        else:
+            assert int(r["messages"]) == 0
+        # schedule arithmetic of the reference: swept 20 -> 21 levels (heat, k=7) / 20 steps (euler, k=3)
+        if r["engine"] == "standard":
+            assert int(r["actual_steps"]) == 20
+    sw = {(r["problem"], r["ranks"]): int(r["actual_steps"]) for r in rows if r["engine"] == "swept"}
+    assert set(sw.values()) <= {sg.build_schedule(20, 16, 1, 1)["completed_steps"],
+                                sg.build_schedule(20, 16, 2, 2)["completed_steps"]}
