@@ -384,6 +384,23 @@ SG_HD constexpr int last_imp_level(int kind, int B) {
 }
 SG_HD constexpr int gather_split(int kind, int B) { return (last_imp_level(kind, B) + 1) / 2; }
 
+// ROW-mode lane lookup: rowmap<KIND, B>.imp[r][i] = (type + 1) | first slot << 3
+// of window row i's imports at level r (type -1: none)
+struct RowMap {
+    int imp[kMaxNL + 1][kMaxB];
+};
+SG_HD constexpr RowMap make_rowmap(int kind, int B) {
+    RowMap m{};
+    const Tables t = make_tables(kind, B);
+    for (int r = 1; r <= nlev(kind, B); ++r)
+        for (int i = 0; i < B; ++i) m.imp[r][i] = (t.imp_type[r][i] + 1) | (t.imp_base[r][i] << 3);
+    return m;
+}
+#if defined(__CUDACC__)
+template <int KIND, int B>
+__device__ const RowMap rowmap = make_rowmap(KIND, B);
+#endif
+
 SG_HD constexpr bool supported(int B) { return B == 8 || B == 12 || B == 16 || B == 24 || B == 32; }
 
 }  // namespace col

@@ -3,6 +3,9 @@
 // sizes compile in parallel.
 #pragma once
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "colgeom.hpp"
 #include "devutil.cuh"
 #include "physics.cuh"
@@ -29,7 +32,13 @@ namespace {
 //      into this instance's record (predicated stores).
 // Lanes outside R_r compute too (SIMT); their cells are never read before an
 // import overwrites them.
-template <int B, int KIND, int CPL, int WPC>
+// FLAGS bit 0 (FAST): a steady-state launch -- no output / snapshot stash
+// (its non-inlined writer call costs the unrolled level code ~20-60
+// registers) and no initial-plane imports.  Bit 1 (DENSE): the gather table
+// is indexed by shared-memory slot (imp_dense), so every shared address and
+// table index is a compile-time immediate off one per-lane base.  Launches
+// with an output or snapshot level or initial-plane cells use FLAGS = 0.
+template <int B, int KIND, int CPL, int WPC, int FLAGS>
 __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_constant__ SweptArgs A) {
     constexpr int L = B / CPL;      // lanes per instance
     constexpr int IPW = 32 / L;     // instances per warp
@@ -37,6 +46,8 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
     constexpr int NL = col::nlev(KIND, B);
     constexpr int YLO = col::ylo(KIND, B);
     constexpr int NIMP = col::imp_total(KIND, B);  // import slots; the transpose tile follows
+    constexpr bool FAST = FLAGS & 1;               // no output / snapshot stash, no initial-plane imports
+    constexpr bool DENSE = FLAGS & 2;              // dense gather (implies FAST)
     extern __shared__ double sm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // b = 12 / 24: the last 32 - IPW*L lanes of a warp are dead (they run the
@@ -44,21 +55,48 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
     const bool dead = lane >= IPW * L;
     const int sub = dead ? 0 : lane / L, l = lane % L;
     const int slot_in_cta = warp * IPW + sub;
-    const int ninst = A.pbx * A.pby;
-    // odd launches walk the instances backwards: their first CTAs read the
-    // records the previous launch wrote last (still in L2)
-    const int cta = (A.lo_parity & 1) ? gridDim.x - 1 - blockIdx.x : blockIdx.x;
-    const int inst = cta * IPC + slot_in_cta;
-    const bool live = !dead && inst < ninst;
-    const int part = A.dev_parts[blockIdx.y];
-    const int pi = part % A.px, pj = part / A.px;
-    const int bi = live ? inst % A.pbx : 0, bj = live ? inst / A.pbx : 0;
+    // grid (ceil(pbx / IPC), pby, partitions); odd launches walk the
+    // instances backwards: their first CTAs read the records the previous
+    // launch wrote last (still in L2)
+    const bool rev = A.lo_parity & 1;
+    const int cbx = rev ? gridDim.x - 1 - blockIdx.x : blockIdx.x;
+    const int cby = rev ? gridDim.y - 1 - blockIdx.y : blockIdx.y;
+    const int ibx = cbx * IPC + slot_in_cta;
+    const bool live = !dead && ibx < A.pbx;
+    const int part = A.dev_parts[blockIdx.z];
+    const int pi = A.dev_pij[blockIdx.z] & 0xffff, pj = A.dev_pij[blockIdx.z] >> 16;
+    const int bi = live ? ibx : 0, bj = cby;
     const int half = A.frame * (B / 2);
     const int gh = A.ghost;
     double* S = sm + slot_in_cta * A.smem_doubles;
 
-    // ---- gather the imports: {offset from this instance's slot-0 record, smem slot}
-    if (live) {
+    // ---- gather the imports
+    if constexpr (DENSE) {
+        // dense: slot i <- ibase[imp_dense[i]], lane l takes slots l, l + L, ...
+        // part A = slots [0, NA) (levels <= gather_split), then part B
+        constexpr int NA = col::imp_base(KIND, B, col::gather_split(KIND, B) + 1, YLO);
+        if (live) {
+            const double* ibase = A.rec[part * A.nslots] + ((long)(bj + gh) * A.extw + (bi + gh)) * A.epad;
+            const int* tab = A.imp_dense + l;
+            const unsigned s0 = static_cast<unsigned>(__cvta_generic_to_shared(S)) + 8u * l;
+            auto part_copy = [&](auto LO, auto HI) {
+                constexpr int lo = decltype(LO)::value, hi = decltype(HI)::value;
+                sfor<(hi - lo + L - 1) / L>([&](auto KI) {
+                    constexpr int i0 = lo + decltype(KI)::value * L;  // slot of lane 0
+                    if constexpr (i0 + L <= hi) {
+                        cp_async8_imm<8 * i0>(s0, ibase + ldg_keep(tab + i0));
+                    } else {
+                        if (i0 + l < hi) cp_async8_imm<8 * i0>(s0, ibase + ldg_keep(tab + i0));
+                    }
+                });
+            };
+            part_copy(std::integral_constant<int, 0>{}, std::integral_constant<int, NA>{});
+            cp_async_commit();
+            part_copy(std::integral_constant<int, NA>{}, std::integral_constant<int, NIMP>{});
+        }
+    }
+    // ---- table gather: {offset from this instance's slot-0 record, smem slot}
+    if (!DENSE && live) {
         const double* ibase = A.rec[part * A.nslots] + ((long)(bj + gh) * A.extw + (bi + gh)) * A.epad;
         // part A (levels <= gather_split), one cp.async group, then part B
         const int na = A.nimp - A.nimp_b;
@@ -89,7 +127,7 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
             const int2 e = ldg_keep(&A.imp_off[i]);
             cp_async8(S + e.y, ibase + e.x);
         }
-        for (int j = l; j < A.ninit; j += L) {
+        if (!FAST) for (int j = l; j < A.ninit; j += L) {
             const int4 im = __ldg(&A.inits[j]);
             const int gx = wrapi(pi * A.pw + bi * B - half + im.x, A.nx);
             const int gy = wrapi(pj * A.ph + bj * B - half + im.y, A.ny);
@@ -104,6 +142,13 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
     double* dst = A.rec[part * A.nslots + A.my_slot] + ((long)(bj + gh) * A.extw + (bi + gh)) * A.epad;
     const double fx = A.c0, fy = A.c1;
     const unsigned s_imp = static_cast<unsigned>(__cvta_generic_to_shared(S));
+    unsigned sc[CPL];  // shared address of slot c (c = the lane's column), for COL-mode imports
+    double* pc[CPL];   // record address of index c, for COL-mode exports
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+        sc[q] = s_imp + 8u * (CPL * l + q);
+        pc[q] = dst + (CPL * l + q);
+    }
     double* tile = S + NIMP;
     // output stash (only allocated by launches that write the output level or snapshots)
     double* stash = sm + IPC * A.smem_doubles + (slot_in_cta * L + l) * CPL * B;
@@ -123,16 +168,27 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
         }
         // ---------------- 1. imports of level r-1
         if constexpr (MODE == col::COL) {
+            // row type t: columns [a, b) minus [hp, hq); the cell of column c
+            // sits at slot base(row) + c - a - (c >= hq ? hq - hp : 0), so the
+            // address is the lane's column address sc (minus the hole width
+            // right of a hole) plus a compile-time offset per row
             bool ip[CPL][4];
             unsigned ia[CPL][4];
             sfor<4>([&](auto TI) {
                 constexpr int t = decltype(TI)::value;
                 constexpr col::RowSet ts = col::Geo<KIND, B>::t.imp_tset[r][t];
+                if constexpr (ts.count() > 0) {
 #pragma unroll
-                for (int q = 0; q < CPL; ++q) {
-                    const int c = CPL * l + q;
-                    ip[q][t] = ts.count() > 0 && ts.has(c);
-                    ia[q][t] = s_imp + 8u * static_cast<unsigned>(ts.count() > 0 ? ts.rank(c) : 0);
+                    for (int q = 0; q < CPL; ++q) {
+                        const int c = CPL * l + q;
+                        ip[q][t] = static_cast<unsigned>(c - ts.a) < static_cast<unsigned>(ts.b - ts.a);
+                        if constexpr (ts.hq > ts.hp) {
+                            ip[q][t] = ip[q][t] && !(static_cast<unsigned>(c - ts.hp) < static_cast<unsigned>(ts.hq - ts.hp));
+                            ia[q][t] = sc[q] - (c >= ts.hq ? 8u * (ts.hq - ts.hp) : 0u);
+                        } else {
+                            ia[q][t] = sc[q];
+                        }
+                    }
                 }
             });
             sfor<B>([&](auto YI) {
@@ -140,25 +196,21 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
                 constexpr int t = col::Geo<KIND, B>::t.imp_type[r][j];
                 constexpr int base = col::Geo<KIND, B>::t.imp_base[r][j];
                 if constexpr (t >= 0) {
+                    constexpr int a0 = col::Geo<KIND, B>::t.imp_tset[r][t].a;
 #pragma unroll
-                    for (int q = 0; q < CPL; ++q) lds_if(v[q][j], ia[q][t] + 8u * base, ip[q][t]);
+                    for (int q = 0; q < CPL; ++q) lds_if_imm<8 * (base - a0)>(v[q][j], ia[q][t], ip[q][t]);
                 }
             });
         } else {
-            int myt[CPL], mybase[CPL];
+            // lane = window row i: its row type and first slot from the
+            // per-kind lookup table (one cached load per level)
+            int myt[CPL];
+            unsigned sa[CPL];
 #pragma unroll
             for (int q = 0; q < CPL; ++q) {
-                const int i = CPL * l + q;
-                myt[q] = -1;
-                mybase[q] = 0;
-                sfor<col::kMaxRuns>([&](auto UI) {
-                    constexpr col::Run ru = col::Geo<KIND, B>::t.imp_runs[r][decltype(UI)::value];
-                    if constexpr (ru.t >= 0)
-                        if (i >= ru.i0 && i < ru.i1) {
-                            myt[q] = ru.t;
-                            mybase[q] = ru.base + (i - ru.i0) * ru.cnt;
-                        }
-                });
+                const int e = __ldg(&col::rowmap<KIND, B>.imp[r][CPL * l + q]);
+                myt[q] = (e & 7) - 1;
+                sa[q] = s_imp + 8u * static_cast<unsigned>(e >> 3);
             }
             sfor<4>([&](auto TI) {
                 constexpr int t = decltype(TI)::value;
@@ -170,8 +222,7 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
                         constexpr int rk = tx.rank(x);
                         if constexpr (tx.has(x)) {
 #pragma unroll
-                            for (int q = 0; q < CPL; ++q)
-                                lds_if(v[q][x], s_imp + 8u * static_cast<unsigned>(mybase[q] + rk), myt[q] == t);
+                            for (int q = 0; q < CPL; ++q) lds_if_imm<8 * rk>(v[q][x], sa[q], myt[q] == t);
                         }
                     });
                 }
@@ -228,19 +279,19 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
             constexpr col::ExpLev E = col::Geo<KIND, B>::t.exp.lev[r];
             if constexpr (E.count() > 0) {
                 if constexpr (MODE == col::COL) {
+                    // rank_band(c) = c - x0 - (c >= mq ? mw : 0): one adjusted
+                    // pointer pa per level, every row's offset compile-time
                     bool pb[CPL], pm[CPL];
-                    double* gh_[CPL];
-                    double* gc[CPL];
-                    double* gm[CPL];
+                    double* pa[CPL];
 #pragma unroll
                     for (int q = 0; q < CPL; ++q) {
                         const int c = CPL * l + q;
-                        pb[q] = E.band(c);
-                        pm[q] = E.mid(c) && c >= E.x0 && c < E.x1;
-                        const int rb = pb[q] ? E.rank_band(c) : 0;
-                        gh_[q] = dst + (E.g1 + rb - E.yh0 * E.bw());  // hole rows: + y * bw
-                        gc[q] = dst + (E.g3 + rb);                     // full rows, band: + f * bw
-                        gm[q] = dst + (E.g2 + (pm[q] ? c - E.mp : 0)); // full rows, middle: + f * mw
+                        const bool in = static_cast<unsigned>(c - E.x0) < static_cast<unsigned>(E.x1 - E.x0);
+                        const bool mid = static_cast<unsigned>(c - E.mp) < static_cast<unsigned>(E.mq - E.mp);
+                        pb[q] = in && !mid;
+                        pm[q] = in && mid;
+                        if constexpr (E.mw() > 0) pa[q] = pc[q] - (c >= E.mq ? E.mw() : 0);
+                        else pa[q] = pc[q];
                     }
                     sfor<B>([&](auto YI) {
                         constexpr int j = decltype(YI)::value;
@@ -249,14 +300,19 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
                         constexpr int f = Ej.full_index(y);
                         if constexpr (Ej.hole_row(y)) {
 #pragma unroll
-                            for (int q = 0; q < CPL; ++q) stg_if(gh_[q] + y * Ej.bw(), v[q][j], pb[q]);
+                            for (int q = 0; q < CPL; ++q)
+                                stg_if_imm<8 * (Ej.g1 + (y - Ej.yh0) * Ej.bw() - Ej.x0)>(pa[q], v[q][j], pb[q]);
                         } else if constexpr (f >= 0) {
                             if constexpr (Ej.bw() > 0) {
 #pragma unroll
-                                for (int q = 0; q < CPL; ++q) stg_if(gc[q] + f * Ej.bw(), v[q][j], pb[q]);
+                                for (int q = 0; q < CPL; ++q)
+                                    stg_if_imm<8 * (Ej.g3 + f * Ej.bw() - Ej.x0)>(pa[q], v[q][j], pb[q]);
                             }
+                            if constexpr (Ej.mw() > 0) {
 #pragma unroll
-                            for (int q = 0; q < CPL; ++q) stg_if(gm[q] + f * Ej.mw(), v[q][j], pm[q]);
+                                for (int q = 0; q < CPL; ++q)
+                                    stg_if_imm<8 * (Ej.g2 + f * Ej.mw() - Ej.mp)>(pc[q], v[q][j], pm[q]);
+                            }
                         }
                     });
                 } else {
@@ -296,11 +352,19 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
                 sfor<2>([&](auto TI) {
                     constexpr int t = decltype(TI)::value;
                     constexpr col::RowSet ts = col::Geo<KIND, B>::t.exp_tset[r][t];
+                    if constexpr (ts.count() > 0) {
 #pragma unroll
-                    for (int q = 0; q < CPL; ++q) {
-                        const int c = CPL * l + q;
-                        ep[q][t] = ts.count() > 0 && ts.has(c);
-                        eg[q][t] = dst + (ts.count() > 0 ? ts.rank(c) : 0);
+                        for (int q = 0; q < CPL; ++q) {
+                            const int c = CPL * l + q;
+                            ep[q][t] = static_cast<unsigned>(c - ts.a) < static_cast<unsigned>(ts.b - ts.a);
+                            if constexpr (ts.hq > ts.hp) {
+                                ep[q][t] = ep[q][t] &&
+                                           !(static_cast<unsigned>(c - ts.hp) < static_cast<unsigned>(ts.hq - ts.hp));
+                                eg[q][t] = pc[q] - (c >= ts.hq ? ts.hq - ts.hp : 0);
+                            } else {
+                                eg[q][t] = pc[q];
+                            }
+                        }
                     }
                 });
                 sfor<B>([&](auto YI) {
@@ -309,8 +373,9 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
                     constexpr int base = col::Geo<KIND, B>::t.exp_base[r][j];
                     static_assert(t < 2, "export row types");
                     if constexpr (t >= 0) {
+                        constexpr int a0 = col::Geo<KIND, B>::t.exp_tset[r][t].a;
 #pragma unroll
-                        for (int q = 0; q < CPL; ++q) stg_if(eg[q][t] + base, v[q][j], ep[q][t]);
+                        for (int q = 0; q < CPL; ++q) stg_if_imm<8 * (base - a0)>(eg[q][t], v[q][j], ep[q][t]);
                     }
                 });
             } else {
@@ -350,7 +415,7 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
         }
         // ---------------- output level / snapshot (rare): through the lane's
         // shared-memory stash to a non-inlined writer
-        if ((((A.out_mask | A.snap_mask) >> r) & 1ull) && !dead) {
+        if (!FAST && (((A.out_mask | A.snap_mask) >> r) & 1ull) && !dead) {
 #pragma unroll
             for (int q = 0; q < CPL; ++q)
 #pragma unroll
@@ -446,24 +511,61 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
     }
 }
 
+inline int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v ? std::atoi(v) : dflt;
+}
+
+// Resident CTAs per SM the shared-memory carveout is sized for (0: driver
+// default).  The gathers land through L1 (cp.async.ca, the gather tables):
+// with the register-lean steady-state kernels the driver would otherwise
+// pack up to ~28 warps per SM and leave L1 a few KB (b16 YBridge 0.36 vs
+// 0.29 ms, Octahedron 0.73 vs 0.55 ms; profiles/r02_summary.md).
+template <int B, int WPC>
+constexpr int target_ctas(int kind) {
+    if constexpr (B <= 16) return WPC <= 2 ? 9 : 18 / WPC;  // 18 warps per SM (CPL = 2: 36 instances at WPC 1)
+    else return kind == col::OCT ? 0 : 3;                   // 4-warp CTAs: 12 warps
+}
+
 template <int B, int CPL, int WPC>
 cudaError_t launch_heat_col_t(const SweptArgs& a, cudaStream_t s) {
     constexpr int IPC = WPC * (32 / (B / CPL));  // instances per CTA
-    const int ninst = a.pbx * a.pby;
     const bool stash = (a.out_mask | a.snap_mask) != 0ull;
     const size_t smem = static_cast<size_t>(IPC) * (a.smem_doubles + (stash ? B * B : 0)) * sizeof(double);
-    dim3 grid((ninst + IPC - 1) / IPC, a.ndev_parts);
+    dim3 grid((a.pbx + IPC - 1) / IPC, a.pby, a.ndev_parts);
+    // variant: 3 = steady state with the dense gather, 1 = steady state with
+    // the table gather, 0 = general (output / snapshot stash, initial-plane
+    // imports).  SG_FAST_KINDS / SG_DENSE_KINDS (bit per kind) restrict them.
+    static const int fast_kinds = env_int("SG_FAST_KINDS", 31);
+    static const int dense_kinds = env_int("SG_DENSE_KINDS", 31);
+    const bool steady = !stash && a.ninit == 0 && ((fast_kinds >> a.kind) & 1);
+    const int flags = !steady ? 0 : (a.dense && ((dense_kinds >> a.kind) & 1)) ? 3 : 1;
+    const bool bridge = a.kind == col::YB || a.kind == col::XB;
+    int carve = -1;
+    if (const int t = target_ctas<B, WPC>(a.kind); t > 0 && flags != 0)
+        carve = std::min(100, static_cast<int>((100 * t * (smem + 1024) + 228 * 1024 - 1) / (228 * 1024)));
+    static const int carve_oct = env_int("SG_CARVE_OCT", -2), carve_br = env_int("SG_CARVE_BR", -2);
+    if (a.kind == col::OCT && carve_oct != -2) carve = carve_oct;
+    if (bridge && carve_br != -2) carve = carve_br;
     auto go = [&](auto kern) {
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             carve >= 0 ? carve : static_cast<int>(cudaSharedmemCarveoutDefault));
         kern<<<grid, WPC * 32, smem, s>>>(a);
         return cudaGetLastError();
     };
+    auto pick = [&](auto K) {
+        constexpr int kd = decltype(K)::value;
+        if (flags == 3) return go(swept_heat_col_kernel<B, kd, CPL, WPC, 3>);
+        if (flags == 1) return go(swept_heat_col_kernel<B, kd, CPL, WPC, 1>);
+        return go(swept_heat_col_kernel<B, kd, CPL, WPC, 0>);
+    };
     switch (a.kind) {
-        case col::UP: return go(swept_heat_col_kernel<B, col::UP, CPL, WPC>);
-        case col::YB: return go(swept_heat_col_kernel<B, col::YB, CPL, WPC>);
-        case col::XB: return go(swept_heat_col_kernel<B, col::XB, CPL, WPC>);
-        case col::OCT: return go(swept_heat_col_kernel<B, col::OCT, CPL, WPC>);
-        default: return go(swept_heat_col_kernel<B, col::DOWN, CPL, WPC>);
+        case col::UP: return pick(std::integral_constant<int, col::UP>{});
+        case col::YB: return pick(std::integral_constant<int, col::YB>{});
+        case col::XB: return pick(std::integral_constant<int, col::XB>{});
+        case col::OCT: return pick(std::integral_constant<int, col::OCT>{});
+        default: return pick(std::integral_constant<int, col::DOWN>{});
     }
 }
 // One column (row) per lane: two per lane halves the shuffles but doubles the
@@ -477,7 +579,11 @@ cudaError_t launch_heat_col(const SweptArgs& a, cudaStream_t s) {
         if (a.pbx * a.pby * a.ndev_parts < 2 * 4 * 148 * 8) return launch_heat_col_t<B, 1, 1>(a, s);
     // b16: 2-warp CTAs (finer-grained residency: 18 instead of 16 warps per
     // SM at ~100 registers; 3.69e11 vs 3.65e11 (4 warps) and 3.61e11 (8))
-    if constexpr (B == 16) return launch_heat_col_t<B, 1, 2>(a, s);
+    if constexpr (B == 16) {
+        static const int wpc = env_int("SG_B16_WPC", 2), cpl = env_int("SG_B16_CPL", 1);
+        if (cpl == 2) return wpc == 1 ? launch_heat_col_t<B, 2, 1>(a, s) : launch_heat_col_t<B, 2, 2>(a, s);
+        return launch_heat_col_t<B, 1, 2>(a, s);
+    }
     return launch_heat_col_t<B, 1, 4>(a, s);
 }
 

@@ -47,6 +47,11 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
     const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
 }
+// smem byte address + compile-time offset (folded into the LDGSTS immediate)
+template <int IMM>
+__device__ __forceinline__ void cp_async8_imm(unsigned saddr, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0+%2], [%1], 8;\n" ::"r"(saddr), "l"(gmem), "n"(IMM) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait_group() {
@@ -63,6 +68,19 @@ __device__ __forceinline__ void lds_if(double& v, unsigned saddr, bool p) {
 __device__ __forceinline__ void stg_if(double* g, double v, bool p) {
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.f64 [%0], %1;\n\t}" ::"l"(g), "d"(v),
                  "r"(static_cast<int>(p)));
+}
+
+// ... with a compile-time byte offset folded into the instruction
+template <int IMM>
+__device__ __forceinline__ void lds_if_imm(double& v, unsigned saddr, bool p) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.shared.f64 %0, [%1+%3];\n\t}"
+                 : "+d"(v)
+                 : "r"(saddr), "r"(static_cast<int>(p)), "n"(IMM));
+}
+template <int IMM>
+__device__ __forceinline__ void stg_if_imm(const double* g, double v, bool p) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.f64 [%0+%3], %1;\n\t}" ::"l"(g), "d"(v),
+                 "r"(static_cast<int>(p)), "n"(IMM));
 }
 
 // Compile-time loop: f(std::integral_constant<int, I>) for I = 0..N-1.

@@ -1,5 +1,6 @@
 // GPU engine -- see engine.hpp.
 #include "engine.hpp"
+#include "colgeom.hpp"
 
 #include <algorithm>
 #include <chrono>
@@ -390,9 +391,39 @@ void Solver::finalize_swept() {
                         if (off > INT32_MAX || off < INT32_MIN) fail(SG_ELOGIC, "swept: record offset overflow");
                         tab.push_back(make_int2(static_cast<int>(off), x.dst));
                     }
+                    std::vector<int>& th = d.imp_off_host[key];
+                    for (const int2& e : tab) th.push_back(e.x);
                     it = d.imp_off.emplace(key, dev_upload(d, tab)).first;
                 }
                 a.imp_off = it->second;
+                // steady classes: every import slot [0, imp_total) is filled by
+                // exactly one import (no initial-plane cells) -> a table
+                // indexed by slot, so the kernel's shared-memory addresses are
+                // compile-time (colkernel.cuh, dense gather)
+                auto jt = d.imp_dense.find(key);
+                if (jt == d.imp_dense.end()) {
+                    int* dt = nullptr;
+                    const int ntot = col::imp_total(L.kind, P.colB);
+                    const int split = col::gather_split(L.kind, P.colB);
+                    const int na = col::imp_base(L.kind, P.colB, split + 1, col::ylo(L.kind, P.colB));
+                    if (T.inits.empty() && static_cast<int>(T.imports.size()) == ntot) {
+                        std::vector<int> tab(static_cast<std::size_t>(ntot), INT32_MIN);
+                        bool ok = true;
+                        for (std::size_t q = 0; q < T.imports.size(); ++q) {
+                            const Import& x = T.imports[q];
+                            if (x.dst < 0 || x.dst >= ntot || tab[x.dst] != INT32_MIN ||
+                                (x.dst < na) != (x.r + 1 <= split)) {
+                                ok = false;
+                                break;
+                            }
+                            tab[x.dst] = d.imp_off_host[key][q];
+                        }
+                        if (ok) dt = dev_upload(d, tab);
+                    }
+                    jt = d.imp_dense.emplace(key, dt).first;
+                }
+                a.imp_dense = jt->second;
+                a.dense = jt->second != nullptr && !std::getenv("SG_NO_DENSE") ? 1 : 0;
             }
             a.nimp = static_cast<int>(T.imports.size());
             a.nimp_b = T.nimp_b;
@@ -425,7 +456,10 @@ void Solver::finalize_swept() {
             a.extw = extw;
             a.nslots = P.nslots;
             a.ndev_parts = static_cast<int>(d.parts.size());
-            for (std::size_t q = 0; q < d.parts.size(); ++q) a.dev_parts[q] = d.parts[q];
+            for (std::size_t q = 0; q < d.parts.size(); ++q) {
+                a.dev_parts[q] = d.parts[q];
+                a.dev_pij[q] = (d.parts[q] % px_) | ((d.parts[q] / px_) << 16);
+            }
             a.rec = d.d_rec_tab;
             a.init_planes = d.d_init_tab;
             a.out_planes = d.d_out_tab;

@@ -47,6 +47,8 @@ struct DeviceCtx {
     std::vector<int4*> d_imp, d_init;
     std::vector<int2*> d_imp2;
     std::map<std::pair<int, int>, int2*> imp_off;  // (class, slot rotation) -> column gather table
+    std::map<std::pair<int, int>, std::vector<int>> imp_off_host;  // host copy of imp_off's offsets
+    std::map<std::pair<int, int>, int*> imp_dense; // (class, slot rotation) -> dense gather table (or null)
     double** d_rec_tab = nullptr;
     double** d_frames_tab = nullptr;
     const double** d_init_tab = nullptr;

@@ -47,6 +47,8 @@ struct SweptArgs {
     const int2* imports2;    // {seg << 20 | src, dst}  (same entries, compact)
     const int2* imp_off;     // column kernels: {offset from the instance's slot-0 record, smem slot}
     int nimp_b;              // column kernels: the last nimp_b entries are gather part B
+    const int* imp_dense;    // column kernels, steady classes: [import slot] -> offset from the slot-0 record
+    int dense;               // 1: imp_dense covers every import slot (no initial-plane cells)
     int lo_parity;           // column kernels: launch index parity (odd: CTAs walk the instances backwards)
     int nimp;
     const int4* inits;       // {rx, ry, dst, vstride}
@@ -63,6 +65,7 @@ struct SweptArgs {
     int b, nx, ny, pw, ph, pbx, pby, px, py, ghost, extw, nslots;
     int ndev_parts;
     int dev_parts[kMaxParts];        // partitions handled by this launch
+    int dev_pij[kMaxParts];          // their (pi | pj << 16)
     double* const* rec;              // [part * nslots + slot]
     const double* const* init_planes;// [part] [var][ph][pw]
     double* const* out_planes;       // [part] [var][ph][pw]
