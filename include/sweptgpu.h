@@ -186,6 +186,13 @@ int sg_plan_info(int problem, int block, long steps, long* stats, char* text, si
  * the FP64 roofline; no reference counterpart. */
 double sg_measure_fp64_peak(void);
 
+/* Self-test of the shared-reciprocal IEEE division the Euler kernels use
+ * (physics.cuh div_dn): bitwise mismatches against x / y over n operand pairs
+ * (random bit patterns incl. zeros, subnormals, infinities, NaNs, and
+ * physical magnitudes); the first mismatching pair goes to xy_bad[0..1].
+ * -1 without a device.  Diagnostic; no reference counterpart. */
+long sg_div_selftest(long n, unsigned long long seed, double* xy_bad);
+
 /* Plan arithmetic, geometry.cpp:59-66 and 169-184.  Returns k / m or -1. */
 int sg_max_levels(int block, int halo);
 long sg_schedule(long requested_steps, int block, int halo, int substeps, long* flat_level);

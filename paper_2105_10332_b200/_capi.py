@@ -53,6 +53,7 @@ EXPORTS = (
     "sg_solver_reset", "sg_solver_solve", "sg_solver_fetch", "sg_solver_kernel_stats",
     "sg_solver_upload", "sg_solver_download", "sg_solver_initial", "sg_solver_set_profile", "sg_solver_destroy", "sg_plan_info", "sg_max_levels", "sg_schedule",
     "sg_measure_fp64_peak",
+    "sg_div_selftest",
     "sg_substep", "sg_fnv1a64", "sg_version", "sg_device_count", "sg_dist_create", "sg_dist_blob", "sg_dist_connect",
 )
 
@@ -93,6 +94,8 @@ def load() -> C.CDLL:
     L.sg_max_levels.argtypes = [C.c_int, C.c_int]
     L.sg_measure_fp64_peak.argtypes = []
     L.sg_measure_fp64_peak.restype = C.c_double
+    L.sg_div_selftest.argtypes = [C.c_long, C.c_uint64, C.POINTER(C.c_double)]
+    L.sg_div_selftest.restype = C.c_long
     L.sg_schedule.argtypes = [C.c_long, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_long)]
     L.sg_schedule.restype = C.c_long
     L.sg_substep.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int,

@@ -200,6 +200,8 @@ void sg_free_result(sg_result* r) {
 
 double sg_measure_fp64_peak(void) { return sg::measure_fp64_peak(); }
 
+long sg_div_selftest(long n, unsigned long long seed, double* xy_bad) { return sg::div_selftest(n, seed, xy_bad); }
+
 int sg_max_levels(int block, int halo) {
     try {
         return sg::max_levels(block, halo);

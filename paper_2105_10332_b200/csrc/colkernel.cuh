@@ -48,6 +48,7 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
     constexpr int NIMP = col::imp_total(KIND, B);  // import slots; the transpose tile follows
     constexpr bool FAST = FLAGS & 1;               // no output / snapshot stash, no initial-plane imports
     constexpr bool DENSE = FLAGS & 2;              // dense gather (implies FAST)
+    constexpr bool REGS = FLAGS & 4;               // dense gather through registers (implies DENSE)
     extern __shared__ double sm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // b = 12 / 24: the last 32 - IPW*L lanes of a warp are dead (they run the
@@ -71,7 +72,34 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
     double* S = sm + slot_in_cta * A.smem_doubles;
 
     // ---- gather the imports
-    if constexpr (DENSE) {
+    // REGS: part A through registers (LDG, then STS: an LDGSTS writes shared
+    // memory one 32-byte sector per wavefront, an STS.64 of a warp 128 bytes),
+    // part B stays in registers until level gather_split + 1
+    constexpr int NA_ = col::imp_base(KIND, B, col::gather_split(KIND, B) + 1, YLO);
+    constexpr int KA = (NA_ + L - 1) / L, KB = (NIMP - NA_ + L - 1) / L;
+    double gbuf[REGS ? (KB > 0 ? KB : 1) : 1];
+    const unsigned s0r = static_cast<unsigned>(__cvta_generic_to_shared(S)) + 8u * l;
+    if constexpr (REGS) if (!dead) {
+        const double* ibase = A.rec[part * A.nslots] + ((long)(bj + gh) * A.extw + (bi + gh)) * A.epad;
+        const int* tab = A.imp_dense + l;
+        double ga[KA > 0 ? KA : 1];
+        sfor<KA>([&](auto KI) {
+            constexpr int i0 = decltype(KI)::value * L;
+            if constexpr (i0 + L <= NA_) ga[decltype(KI)::value] = __ldg(ibase + ldg_keep(tab + i0));
+            else if (i0 + l < NA_) ga[decltype(KI)::value] = __ldg(ibase + ldg_keep(tab + i0));
+        });
+        sfor<KB>([&](auto KI) {
+            constexpr int i0 = NA_ + decltype(KI)::value * L;
+            if constexpr (i0 + L <= NIMP) gbuf[decltype(KI)::value] = __ldg(ibase + ldg_keep(tab + i0));
+            else if (i0 + l < NIMP) gbuf[decltype(KI)::value] = __ldg(ibase + ldg_keep(tab + i0));
+        });
+        sfor<KA>([&](auto KI) {
+            constexpr int i0 = decltype(KI)::value * L;
+            if constexpr (i0 + L <= NA_) sts_imm<8 * i0>(s0r, ga[decltype(KI)::value]);
+            else if (i0 + l < NA_) sts_imm<8 * i0>(s0r, ga[decltype(KI)::value]);
+        });
+    }
+    if constexpr (DENSE && !REGS) {
         // dense: slot i <- ibase[imp_dense[i]], lane l takes slots l, l + L, ...
         // part A = slots [0, NA) (levels <= gather_split), then part B
         constexpr int NA = col::imp_base(KIND, B, col::gather_split(KIND, B) + 1, YLO);
@@ -163,7 +191,15 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
         constexpr int MODE = col::mode(KIND, B, r);
         constexpr col::CRect q0 = col::rect(KIND, B, r);
         if constexpr (r == col::gather_split(KIND, B) + 1) {
-            cp_async_wait_all();  // part B
+            if constexpr (REGS) {
+                if (!dead) sfor<KB>([&](auto KI) {
+                    constexpr int i0 = NA_ + decltype(KI)::value * L;
+                    if constexpr (i0 + L <= NIMP) sts_imm<8 * i0>(s0r, gbuf[decltype(KI)::value]);
+                    else if (i0 + l < NIMP) sts_imm<8 * i0>(s0r, gbuf[decltype(KI)::value]);
+                });
+            } else {
+                cp_async_wait_all();  // part B
+            }
             __syncwarp();
         }
         // ---------------- 1. imports of level r-1
@@ -539,7 +575,12 @@ cudaError_t launch_heat_col_t(const SweptArgs& a, cudaStream_t s) {
     static const int fast_kinds = env_int("SG_FAST_KINDS", 31);
     static const int dense_kinds = env_int("SG_DENSE_KINDS", 31);
     const bool steady = !stash && a.ninit == 0 && ((fast_kinds >> a.kind) & 1);
-    const int flags = !steady ? 0 : (a.dense && ((dense_kinds >> a.kind) & 1)) ? 3 : 1;
+    // b32: the Octahedron's part A through registers (b32 1.25 vs 1.34 ms;
+    // at b16 the LDGSTS path is faster: 0.56 vs 0.67 ms)
+    static const int reg_kinds = env_int("SG_REG_KINDS", B == 32 ? (1 << col::OCT) : 0);
+    const int flags = !steady ? 0
+                      : (a.dense && ((dense_kinds >> a.kind) & 1)) ? (((reg_kinds >> a.kind) & 1) ? 7 : 3)
+                                                                   : 1;
     const bool bridge = a.kind == col::YB || a.kind == col::XB;
     int carve = -1;
     if (const int t = target_ctas<B, WPC>(a.kind); t > 0 && flags != 0)
@@ -556,6 +597,7 @@ cudaError_t launch_heat_col_t(const SweptArgs& a, cudaStream_t s) {
     };
     auto pick = [&](auto K) {
         constexpr int kd = decltype(K)::value;
+        if (flags == 7) return go(swept_heat_col_kernel<B, kd, CPL, WPC, 7>);
         if (flags == 3) return go(swept_heat_col_kernel<B, kd, CPL, WPC, 3>);
         if (flags == 1) return go(swept_heat_col_kernel<B, kd, CPL, WPC, 1>);
         return go(swept_heat_col_kernel<B, kd, CPL, WPC, 0>);
@@ -580,8 +622,6 @@ cudaError_t launch_heat_col(const SweptArgs& a, cudaStream_t s) {
     // b16: 2-warp CTAs (finer-grained residency: 18 instead of 16 warps per
     // SM at ~100 registers; 3.69e11 vs 3.65e11 (4 warps) and 3.61e11 (8))
     if constexpr (B == 16) {
-        static const int wpc = env_int("SG_B16_WPC", 2), cpl = env_int("SG_B16_CPL", 1);
-        if (cpl == 2) return wpc == 1 ? launch_heat_col_t<B, 2, 1>(a, s) : launch_heat_col_t<B, 2, 2>(a, s);
         return launch_heat_col_t<B, 1, 2>(a, s);
     }
     return launch_heat_col_t<B, 1, 4>(a, s);

@@ -83,6 +83,11 @@ __device__ __forceinline__ void stg_if_imm(const double* g, double v, bool p) {
                  "r"(static_cast<int>(p)), "n"(IMM));
 }
 
+template <int IMM>
+__device__ __forceinline__ void sts_imm(unsigned saddr, double v) {
+    asm volatile("st.shared.f64 [%0+%2], %1;" ::"r"(saddr), "d"(v), "n"(IMM) : "memory");
+}
+
 // Compile-time loop: f(std::integral_constant<int, I>) for I = 0..N-1.
 template <class F, int... I>
 __device__ __forceinline__ void sfor_impl(F&& f, std::integer_sequence<int, I...>) {

@@ -752,6 +752,61 @@ double measure_fp64_peak() {
     return 2.0 * 8.0 * iters * blocks * 256.0 / (best * 1e-3);
 }
 
+// div_dn self-test: operands are random bit patterns (every exponent,
+// zeros, subnormals, infinities, NaNs included) plus, every fourth pair,
+// "physical" operands (the magnitudes the Euler fluxes divide); a mismatch is
+// any pair where div_dn(x, y, recip_dn(y)) and x / y differ in bits (two NaNs
+// count as equal).
+__device__ __forceinline__ unsigned long long splitmix64(unsigned long long& s) {
+    unsigned long long z = (s += 0x9e3779b97f4a7c15ull);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+__global__ void div_selftest_kernel(long n, unsigned long long seed, unsigned long long* bad,
+                                    double* first_bad) {
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        unsigned long long st = seed ^ (0x632be59bd9b4e019ull * (unsigned long long)(i + 1));
+        const unsigned long long a = splitmix64(st), b = splitmix64(st);
+        double x = __longlong_as_double((long long)a), y = __longlong_as_double((long long)b);
+        if ((i & 3) == 3) {  // physical magnitudes: x in +-[1e-3, 1e3], y in [1e-2, 1e2]
+            x = (a & 1 ? -1.0 : 1.0) * exp10(-3.0 + 6.0 * ((a >> 11) * 0x1.0p-53));
+            y = exp10(-2.0 + 4.0 * ((b >> 11) * 0x1.0p-53));
+        }
+        if ((i & 255) == 7) y = 0.0;
+        if ((i & 255) == 9) x = 0.0;
+        const double q1 = x / y, q2 = div_dn(x, y, recip_dn(y));
+        const bool same = __double_as_longlong(q1) == __double_as_longlong(q2) || (isnan(q1) && isnan(q2));
+        if (!same) {
+            if (atomicAdd(bad, 1ull) == 0ull) {
+                first_bad[0] = x;
+                first_bad[1] = y;
+            }
+        }
+    }
+}
+
+long div_selftest(long n, unsigned long long seed, double* xy_bad) {
+    unsigned long long* bad = nullptr;
+    double* fb = nullptr;
+    if (cudaMalloc(&bad, sizeof(unsigned long long)) != cudaSuccess) return -1;
+    if (cudaMalloc(&fb, 2 * sizeof(double)) != cudaSuccess) return -1;
+    cudaMemset(bad, 0, sizeof(unsigned long long));
+    div_selftest_kernel<<<148 * 16, 256>>>(n, seed, bad, fb);
+    unsigned long long h = 0;
+    double hb[2] = {0, 0};
+    const bool ok = cudaMemcpy(&h, bad, sizeof h, cudaMemcpyDeviceToHost) == cudaSuccess &&
+                    cudaMemcpy(hb, fb, sizeof hb, cudaMemcpyDeviceToHost) == cudaSuccess;
+    cudaFree(bad);
+    cudaFree(fb);
+    if (!ok) return -1;
+    if (xy_bad) {
+        xy_bad[0] = hb[0];
+        xy_bad[1] = hb[1];
+    }
+    return static_cast<long>(h);
+}
+
 cudaError_t launch_dist_barrier(unsigned long long* const* peer_flags, unsigned long long* my_flags, int world,
                                 int rank, unsigned long long epoch, int* err, cudaStream_t s) {
     dist_barrier_kernel<<<1, 32, 0, s>>>(peer_flags, my_flags, world, rank, epoch, err);

@@ -96,5 +96,8 @@ struct StdArgs {
 
 // FP64 flop/s of the current device without FMA (kernels.cu), -1 on error
 double measure_fp64_peak();
+// div_dn / recip_dn (physics.cuh) against IEEE division on n operand pairs:
+// number of bitwise mismatches (first one in xy_bad[0..1]), -1 on error
+long div_selftest(long n, unsigned long long seed, double* xy_bad);
 
 }  // namespace sg
