@@ -122,8 +122,9 @@ SG_HD constexpr int exp_base_rm(int kind, int B, int r, int y) {
 }
 SG_HD constexpr int imp_total(int kind, int B) { return imp_base(kind, B, nlev(kind, B) + 1, ylo(kind, B)); }
 
-// slot of an imported cell at level r-1 (column x, row y), -1 if not an import
-SG_HD constexpr int imp_slot(int kind, int B, int r, int x, int y) {
+// row-major slot of an imported cell at level r-1 (column x, row y), -1 if
+// not an import (COL-mode levels; imp_slot below picks per level)
+SG_HD constexpr int imp_slot_rm(int kind, int B, int r, int x, int y) {
     if (y < ylo(kind, B) || y >= ylo(kind, B) + B) return -1;
     const RowSet s = imp_row(kind, B, r, y);
     return s.has(x) ? imp_base(kind, B, r, y) + s.rank(x) : -1;
@@ -275,6 +276,59 @@ SG_HD constexpr int mode(int kind, int B, int r) {
     if (empty(q)) return COL;
     return (q.x1 - q.x0) < (q.y1 - q.y0) ? ROW : COL;
 }
+// Imported rows of column x at level r-1 (the transpose of imp_row): ROW-mode
+// levels (lane = window row) store their imports column-major, so that a
+// warp's per-column shared load reads consecutive slots (no bank conflicts)
+// exactly as a COL-mode level's per-row load does.
+SG_HD constexpr RowSet imp_col(int kind, int B, int r, int x) {
+    const CRect q = rect(kind, B, r);
+    if (empty(q)) return RowSet{0, 0, 0, 0};
+    int a = 0, b = 0;
+    if (x >= q.x0 && x < q.x1) {
+        a = q.y0 - 1;
+        b = q.y1 + 1;
+    } else if (x == q.x0 - 1 || x == q.x1) {
+        a = q.y0;
+        b = q.y1;
+    } else {
+        return RowSet{0, 0, 0, 0};
+    }
+    const CRect p = rect(kind, B, r - 1);
+    if (!empty(p) && x >= p.x0 && x < p.x1) return make_row(a, b, p.y0, p.y1);
+    return make_row(a, b, b, b);
+}
+// first slot of column x's imports at a ROW-mode level r (after the level base)
+SG_HD constexpr int imp_cbase(int kind, int B, int r, int x) {
+    int s = imp_base(kind, B, r, ylo(kind, B));
+    for (int xx = 0; xx < x; ++xx) s += imp_col(kind, B, r, xx).count();
+    return s;
+}
+// slot of an imported cell at level r-1 (column x, row y), -1 if not an
+// import: row-major at COL-mode levels, column-major at ROW-mode levels
+SG_HD constexpr int imp_slot(int kind, int B, int r, int x, int y) {
+    if (y < ylo(kind, B) || y >= ylo(kind, B) + B || x < 0 || x >= B) return -1;
+    if (mode(kind, B, r) == COL) return imp_slot_rm(kind, B, r, x, y);
+    const RowSet c = imp_col(kind, B, r, x);
+    return c.has(y) ? imp_cbase(kind, B, r, x) + c.rank(y) : -1;
+}
+
+// both enumerations cover the same cells (checked at compile time by the kernels)
+SG_HD constexpr bool imp_cols_ok(int kind, int B) {
+    for (int r = 1; r <= nlev(kind, B); ++r) {
+        int nr = 0, nc = 0;
+        for (int i = 0; i < B; ++i) {
+            nr += imp_row(kind, B, r, ylo(kind, B) + i).count();
+            nc += imp_col(kind, B, r, i).count();
+            const RowSet c = imp_col(kind, B, r, i);
+            for (int y = c.a; y < c.b; ++y)
+                if (c.has(y) && (y < ylo(kind, B) || y >= ylo(kind, B) + B || !imp_row(kind, B, r, y).has(i)))
+                    return false;
+        }
+        if (nr != nc) return false;
+    }
+    return true;
+}
+
 // transpose tile (cells of R_r at a mode switch after level r), doubles
 SG_HD constexpr int tile_doubles(int kind, int B) {
     int m = 0;
@@ -304,6 +358,10 @@ struct Tables {
     int imp_base[kMaxNL + 2][kMaxB], exp_base[kMaxNL + 2][kMaxB];
     int imp_type[kMaxNL + 1][kMaxB], exp_type[kMaxNL + 1][kMaxB];
     RowSet imp_tset[kMaxNL + 1][4], exp_tset[kMaxNL + 1][2];
+    // ROW-mode levels: imported rows per column, their types and first slots
+    RowSet impc[kMaxNL + 1][kMaxB];
+    int impc_type[kMaxNL + 1][kMaxB], impc_base[kMaxNL + 1][kMaxB];
+    RowSet impc_tset[kMaxNL + 1][4];
     ExpLayout exp;  // grouped layout (b < 32); the exp_* row tables: row-major (b = 32)
 };
 template <int NT>
@@ -361,6 +419,15 @@ SG_HD constexpr Tables make_tables(int kind, int B) {
             }
         }
     fill_types<4>(t.imp, nl, B, t.imp_type, t.imp_tset);
+    for (int r = 1; r <= nl; ++r) {
+        int sc = t.imp_base[r][0];
+        for (int x = 0; x < B; ++x) {
+            t.impc[r][x] = imp_col(kind, B, r, x);
+            t.impc_base[r][x] = sc;
+            sc += t.impc[r][x].count();
+        }
+    }
+    fill_types<4>(t.impc, nl, B, t.impc_type, t.impc_tset);
     fill_types<2>(t.expr, nl, B, t.exp_type, t.exp_tset);
     fill_runs(t.imp_type, t.imp_base, t.imp, nl, B, t.imp_runs);
     fill_runs(t.exp_type, t.exp_base, t.expr, nl, B, t.exp_runs);
@@ -383,23 +450,6 @@ SG_HD constexpr int last_imp_level(int kind, int B) {
     return last;
 }
 SG_HD constexpr int gather_split(int kind, int B) { return (last_imp_level(kind, B) + 1) / 2; }
-
-// ROW-mode lane lookup: rowmap<KIND, B>.imp[r][i] = (type + 1) | first slot << 3
-// of window row i's imports at level r (type -1: none)
-struct RowMap {
-    int imp[kMaxNL + 1][kMaxB];
-};
-SG_HD constexpr RowMap make_rowmap(int kind, int B) {
-    RowMap m{};
-    const Tables t = make_tables(kind, B);
-    for (int r = 1; r <= nlev(kind, B); ++r)
-        for (int i = 0; i < B; ++i) m.imp[r][i] = (t.imp_type[r][i] + 1) | (t.imp_base[r][i] << 3);
-    return m;
-}
-#if defined(__CUDACC__)
-template <int KIND, int B>
-__device__ const RowMap rowmap = make_rowmap(KIND, B);
-#endif
 
 SG_HD constexpr bool supported(int B) { return B == 8 || B == 12 || B == 16 || B == 24 || B == 32; }
 

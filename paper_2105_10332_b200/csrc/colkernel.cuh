@@ -238,29 +238,36 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
                 }
             });
         } else {
-            // lane = window row i: its row type and first slot from the
-            // per-kind lookup table (one cached load per level)
-            int myt[CPL];
-            unsigned sa[CPL];
-#pragma unroll
-            for (int q = 0; q < CPL; ++q) {
-                const int e = __ldg(&col::rowmap<KIND, B>.imp[r][CPL * l + q]);
-                myt[q] = (e & 7) - 1;
-                sa[q] = s_imp + 8u * static_cast<unsigned>(e >> 3);
-            }
+            // lane = window row y: the level's imports are column-major
+            // (colgeom imp_col), the transpose of the COL-mode case above
+            static_assert(col::imp_cols_ok(KIND, B), "imp_col / imp_row disagree");
+            bool ip[CPL][4];
+            unsigned ia[CPL][4];
             sfor<4>([&](auto TI) {
                 constexpr int t = decltype(TI)::value;
-                constexpr col::RowSet ts = col::Geo<KIND, B>::t.imp_tset[r][t];
+                constexpr col::RowSet ts = col::Geo<KIND, B>::t.impc_tset[r][t];
                 if constexpr (ts.count() > 0) {
-                    sfor<B>([&](auto XI) {
-                        constexpr int x = decltype(XI)::value;
-                        constexpr col::RowSet tx = col::Geo<KIND, B>::t.imp_tset[r][t];
-                        constexpr int rk = tx.rank(x);
-                        if constexpr (tx.has(x)) {
 #pragma unroll
-                            for (int q = 0; q < CPL; ++q) lds_if_imm<8 * rk>(v[q][x], sa[q], myt[q] == t);
+                    for (int q = 0; q < CPL; ++q) {
+                        const int y = YLO + CPL * l + q;
+                        ip[q][t] = static_cast<unsigned>(y - ts.a) < static_cast<unsigned>(ts.b - ts.a);
+                        if constexpr (ts.hq > ts.hp) {
+                            ip[q][t] = ip[q][t] && !(static_cast<unsigned>(y - ts.hp) < static_cast<unsigned>(ts.hq - ts.hp));
+                            ia[q][t] = sc[q] - (y >= ts.hq ? 8u * (ts.hq - ts.hp) : 0u);
+                        } else {
+                            ia[q][t] = sc[q];
                         }
-                    });
+                    }
+                }
+            });
+            sfor<B>([&](auto XI) {
+                constexpr int x = decltype(XI)::value;
+                constexpr int t = col::Geo<KIND, B>::t.impc_type[r][x];
+                constexpr int base = col::Geo<KIND, B>::t.impc_base[r][x];
+                if constexpr (t >= 0) {
+                    constexpr int a0 = col::Geo<KIND, B>::t.impc_tset[r][t].a;
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) lds_if_imm<8 * (base - a0 + YLO)>(v[q][x], ia[q][t], ip[q][t]);
                 }
             });
         }
