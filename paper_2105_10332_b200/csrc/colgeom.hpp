@@ -335,7 +335,7 @@ SG_HD constexpr int tile_doubles(int kind, int B) {
     for (int r = 1; r < nlev(kind, B); ++r)
         if (mode(kind, B, r) != mode(kind, B, r + 1)) {
             const CRect q = rect(kind, B, r);
-            const int a = (q.x1 - q.x0) * (q.y1 - q.y0);
+            const int a = ((q.x1 - q.x0) | 1) * (q.y1 - q.y0);  // odd row stride: no bank conflicts
             m = a > m ? a : m;
         }
     return m;

@@ -481,8 +481,10 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
         }
         // ---------------- layout switch after this level: transpose R_r
         if constexpr (r < NL && col::mode(KIND, B, r + 1) != MODE) {
-            constexpr int w = q0.x1 - q0.x0;
-            static_assert(w * (q0.y1 - q0.y0) <= col::tile_doubles(KIND, B), "transpose tile");
+            // tile rows of odd stride ws: the lanes of a row-mode access hit
+            // distinct banks
+            constexpr int ws = (q0.x1 - q0.x0) | 1;
+            static_assert(ws * (q0.y1 - q0.y0) <= col::tile_doubles(KIND, B), "transpose tile");
 #pragma unroll
             for (int q = 0; q < CPL; ++q) {
                 const int m = CPL * l + q;
@@ -492,12 +494,12 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
                         sfor<B>([&](auto YI) {
                             constexpr int j = decltype(YI)::value;
                             constexpr col::CRect qr = col::rect(KIND, B, r);
-                            if constexpr (YLO + j >= qr.y0 && YLO + j < qr.y1) t0[(YLO + j - qr.y0) * w] = v[q][j];
+                            if constexpr (YLO + j >= qr.y0 && YLO + j < qr.y1) t0[(YLO + j - qr.y0) * ws] = v[q][j];
                         });
                     }
                 } else {
                     if (!dead && YLO + m >= q0.y0 && YLO + m < q0.y1) {
-                        double* t0 = tile + (YLO + m - q0.y0) * w;
+                        double* t0 = tile + (YLO + m - q0.y0) * ws;
                         sfor<B>([&](auto XI) {
                             constexpr int x = decltype(XI)::value;
                             constexpr col::CRect qr = col::rect(KIND, B, r);
@@ -512,7 +514,7 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
                 const int m = CPL * l + q;
                 if constexpr (MODE == col::COL) {  // now ROW: m = window row
                     if (YLO + m >= q0.y0 && YLO + m < q0.y1) {
-                        const double* t0 = tile + (YLO + m - q0.y0) * w;
+                        const double* t0 = tile + (YLO + m - q0.y0) * ws;
                         sfor<B>([&](auto XI) {
                             constexpr int x = decltype(XI)::value;
                             constexpr col::CRect qr = col::rect(KIND, B, r);
@@ -525,7 +527,7 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
                         sfor<B>([&](auto YI) {
                             constexpr int j = decltype(YI)::value;
                             constexpr col::CRect qr = col::rect(KIND, B, r);
-                            if constexpr (YLO + j >= qr.y0 && YLO + j < qr.y1) v[q][j] = t0[(YLO + j - qr.y0) * w];
+                            if constexpr (YLO + j >= qr.y0 && YLO + j < qr.y1) v[q][j] = t0[(YLO + j - qr.y0) * ws];
                         });
                     }
                 }
