@@ -34,6 +34,10 @@ def one(rep, idx):
     if len(raw) < 3:
         return None
     d = dict(zip(raw[0], raw[2]))
+    units = dict(zip(raw[0], raw[1]))
+    tscale = {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0}.get(
+        units.get("gpu__time_duration.sum", ""), 1.0)
+    bscale = lambda k: {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(units.get(k, "byte"), 1.0)
     grid = num(d.get("launch__grid_size", "nan"))
     block = num(d.get("launch__block_size", "nan"))
     warps = grid * block / 32
@@ -41,7 +45,7 @@ def one(rep, idx):
     pw = lambda k: round(num(d.get(k, "nan")) / warps, 1)
     out = {
         "kernel": d.get("Kernel Name", "?"),
-        "duration_ms": num(d.get("gpu__time_duration.sum", "nan")),
+        "duration_ms": round(num(d.get("gpu__time_duration.sum", "nan")) * tscale, 4),
         "warps": warps,
         "registers": num(d.get("launch__registers_per_thread", "nan")),
         "instructions_per_warp": pw("smsp__inst_executed.sum"),
@@ -53,7 +57,8 @@ def one(rep, idx):
         "global_st_wavefronts_per_warp": pw("l1tex__t_output_wavefronts_pipe_lsu_mem_global_op_st.sum"),
         "ldgsts_bank_conflicts_per_warp": pw("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ldgsts.sum"),
         "fp64_pipe_pct": round(num(d.get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "nan")), 1),
-        "dram_bytes": num(d.get("dram__bytes_read.sum", "nan")) + num(d.get("dram__bytes_write.sum", "nan")),
+        "dram_bytes": num(d.get("dram__bytes_read.sum", "nan")) * bscale("dram__bytes_read.sum")
+        + num(d.get("dram__bytes_write.sum", "nan")) * bscale("dram__bytes_write.sum"),
     }
     src = ncu_csv(rep, "source", idx, ("--print-source", "sass"))
     hdr, ops, seen = None, collections.Counter(), set()
