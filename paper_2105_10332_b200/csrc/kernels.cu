@@ -752,7 +752,7 @@ double measure_fp64_peak() {
     return 2.0 * 8.0 * iters * blocks * 256.0 / (best * 1e-3);
 }
 
-// div_dn self-test: operands are random bit patterns (every exponent,
+// div_dn / div_nb / sqrt_nb self-test: operands are random bit patterns (every exponent,
 // zeros, subnormals, infinities, NaNs included) plus, every fourth pair,
 // "physical" operands (the magnitudes the Euler fluxes divide); a mismatch is
 // any pair where div_dn(x, y, recip_dn(y)) and x / y differ in bits (two NaNs
@@ -776,7 +776,19 @@ __global__ void div_selftest_kernel(long n, unsigned long long seed, unsigned lo
         if ((i & 255) == 7) y = 0.0;
         if ((i & 255) == 9) x = 0.0;
         const double q1 = x / y, q2 = div_dn(x, y, recip_dn(y));
-        const bool same = __double_as_longlong(q1) == __double_as_longlong(q2) || (isnan(q1) && isnan(q2));
+        bool ok = true;
+        double q3 = div_nb(x, y, recip_dn(y), ok);
+        if (!ok) q3 = x / y;
+        // sqrt: the same operands as |x| (and x itself: negative / NaN cases)
+        const double sa = (i & 1) ? fabs(x) : x;
+        const double s1 = sqrt(sa);
+        bool oks = true;
+        double s2 = sqrt_nb(sa, oks);
+        if (!oks) s2 = sqrt(sa);
+        auto eq = [](double u, double w) {
+            return __double_as_longlong(u) == __double_as_longlong(w) || (isnan(u) && isnan(w));
+        };
+        const bool same = eq(q1, q2) && eq(q1, q3) && eq(s1, s2);
         if (!same) {
             if (atomicAdd(bad, 1ull) == 0ull) {
                 first_bad[0] = x;
@@ -844,7 +856,8 @@ cudaError_t launch_swept(int problem, const SweptArgs& a, cudaStream_t s) {
         // 7 resident CTAs (<= 72 registers): occupancy hides the FP64
         // dependency chains and the per-level barriers (1.09e10 vs 8.5e9
         // updates/s at 112 registers, Euler 960^2 b16)
-        auto kern = swept_euler_kernel<7>;
+        static const int minb = [] { const char* v = std::getenv("SG_EULER_MINB"); return v ? std::atoi(v) : 7; }();
+        auto kern = minb == 5 ? swept_euler_kernel<5> : minb == 6 ? swept_euler_kernel<6> : swept_euler_kernel<7>;
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         dim3 grid(ninst, a.ndev_parts);
         kern<<<grid, 128, smem, s>>>(a);
