@@ -853,10 +853,11 @@ cudaError_t launch_swept(int problem, const SweptArgs& a, cudaStream_t s) {
     }
     {
         const size_t smem = static_cast<size_t>(a.smem_doubles + a.ps_doubles + 2 * a.fx_doubles) * sizeof(double);
-        // 7 resident CTAs (<= 72 registers): occupancy hides the FP64
-        // dependency chains and the per-level barriers (1.09e10 vs 8.5e9
-        // updates/s at 112 registers, Euler 960^2 b16)
-        static const int minb = [] { const char* v = std::getenv("SG_EULER_MINB"); return v ? std::atoi(v) : 7; }();
+        // 6-7 resident CTAs: occupancy hides the FP64 dependency chains and
+        // the per-level barriers (1.09e10 at 72 registers vs 8.5e9 at 112,
+        // Euler 960^2 b16); 6 (<= 80 registers) since the branch-free flux
+        // code: 1.20e10 vs 1.16e10 (7 CTAs, more spills)
+        static const int minb = [] { const char* v = std::getenv("SG_EULER_MINB"); return v ? std::atoi(v) : 6; }();
         auto kern = minb == 5 ? swept_euler_kernel<5> : minb == 6 ? swept_euler_kernel<6> : swept_euler_kernel<7>;
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         dim3 grid(ninst, a.ndev_parts);
