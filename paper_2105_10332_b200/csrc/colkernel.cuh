@@ -49,6 +49,12 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
     constexpr bool FAST = FLAGS & 1;               // no output / snapshot stash, no initial-plane imports
     constexpr bool DENSE = FLAGS & 2;              // dense gather (implies FAST)
     constexpr bool REGS = FLAGS & 4;               // dense gather through registers (implies DENSE)
+    // HALF (FLAGS bits 4-5): 0 = all levels; 1 / 2 = the Octahedron's levels
+    // 1..k / k+1..2k as two launches, the level-k state through oct_scratch
+    constexpr int HALF = (FLAGS >> 4) & 3;
+    constexpr int KO = B / 2 - 1;
+    constexpr int RLO = HALF == 2 ? KO + 1 : 1, RHI = HALF == 1 ? KO : NL;
+    static_assert(HALF == 0 || (KIND == col::OCT && DENSE && !REGS && CPL == 1), "split Octahedron");
     extern __shared__ double sm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // b = 12 / 24: the last 32 - IPW*L lanes of a warp are dead (they run the
@@ -101,8 +107,13 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
     }
     if constexpr (DENSE && !REGS) {
         // dense: slot i <- ibase[imp_dense[i]], lane l takes slots l, l + L, ...
-        // part A = slots [0, NA) (levels <= gather_split), then part B
-        constexpr int NA = col::imp_base(KIND, B, col::gather_split(KIND, B) + 1, YLO);
+        // part A = slots [0, NA) (levels <= gather_split), then part B; a split
+        // Octahedron's halves gather the slots of their own levels only
+        constexpr int NK = col::imp_base(KIND, B, KO + 1, YLO);
+        constexpr int NS = col::imp_base(KIND, B, col::gather_split(KIND, B) + 1, YLO);
+        constexpr int GA0 = HALF == 2 ? NK : 0;
+        constexpr int NA = HALF == 2 ? NIMP : HALF == 1 ? (NS < NK ? NS : NK) : NS;
+        constexpr int NEND = HALF == 1 ? NK : NIMP;
         if (live) {
             const double* ibase = A.rec[part * A.nslots] + ((long)(bj + gh) * A.extw + (bi + gh)) * A.epad;
             const int* tab = A.imp_dense + l;
@@ -118,9 +129,9 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
                     }
                 });
             };
-            part_copy(std::integral_constant<int, 0>{}, std::integral_constant<int, NA>{});
+            part_copy(std::integral_constant<int, GA0>{}, std::integral_constant<int, NA>{});
             cp_async_commit();
-            part_copy(std::integral_constant<int, NA>{}, std::integral_constant<int, NIMP>{});
+            part_copy(std::integral_constant<int, NA>{}, std::integral_constant<int, NEND>{});
         }
     }
     // ---- table gather: {offset from this instance's slot-0 record, smem slot}
@@ -181,13 +192,21 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
     // output stash (only allocated by launches that write the output level or snapshots)
     double* stash = sm + IPC * A.smem_doubles + (slot_in_cta * L + l) * CPL * B;
     double v[CPL][B];
+    // the split Octahedron's level-k state: [dev part][bj][bi][row][lane]
+    double* scr = HALF ? A.oct_scratch + ((((long)blockIdx.z * A.pby + bj) * A.pbx + bi) * B) * B + l : nullptr;
+    if constexpr (HALF == 2) {
 #pragma unroll
-    for (int q = 0; q < CPL; ++q)
+        for (int i = 0; i < B; ++i) v[0][i] = scr[i * B];
+    } else {
 #pragma unroll
-        for (int i = 0; i < B; ++i) v[q][i] = 0.0;
+        for (int q = 0; q < CPL; ++q)
+#pragma unroll
+            for (int i = 0; i < B; ++i) v[q][i] = 0.0;
+    }
 
     sfor<NL>([&](auto RI) {
         constexpr int r = decltype(RI)::value + 1;
+        if constexpr (r >= RLO && r <= RHI) {
         constexpr int MODE = col::mode(KIND, B, r);
         constexpr col::CRect q0 = col::rect(KIND, B, r);
         if constexpr (r == col::gather_split(KIND, B) + 1) {
@@ -534,7 +553,15 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
             }
             __syncwarp();
         }
+        }  // level range (split Octahedron)
     });
+    if constexpr (HALF == 1) {
+        if (live) {
+#pragma unroll
+            for (int i = 0; i < B; ++i) scr[i * B] = v[0][i];
+        }
+        return;  // the second half pushes the partition-edge records
+    }
 
     // ---- partition-edge instances: copy the record into the neighbours' ghost rings
     const bool edge = bi < gh || bi >= A.pbx - gh || bj < gh || bj >= A.pby - gh;
@@ -606,6 +633,13 @@ cudaError_t launch_heat_col_t(const SweptArgs& a, cudaStream_t s) {
     };
     auto pick = [&](auto K) {
         constexpr int kd = decltype(K)::value;
+        if constexpr (B == 32 && kd == col::OCT && CPL == 1) {
+            if (a.oct_scratch && (flags == 3 || flags == 7)) {
+                const cudaError_t e = go(swept_heat_col_kernel<B, kd, CPL, WPC, 3 | 16>);
+                if (e != cudaSuccess) return e;
+                return go(swept_heat_col_kernel<B, kd, CPL, WPC, 3 | 32>);
+            }
+        }
         if (flags == 7) return go(swept_heat_col_kernel<B, kd, CPL, WPC, 7>);
         if (flags == 3) return go(swept_heat_col_kernel<B, kd, CPL, WPC, 3>);
         if (flags == 1) return go(swept_heat_col_kernel<B, kd, CPL, WPC, 1>);

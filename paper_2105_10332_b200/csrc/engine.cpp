@@ -328,6 +328,11 @@ void Solver::finalize_swept() {
             d.d_imp.push_back(dev_upload(d, im));
             d.d_init.push_back(dev_upload(d, in));
         }
+        // b32: the Octahedron runs as two launches (levels 1..k, k+1..2k) so
+        // each kernel's straight-line code is half as long (instruction
+        // fetch bound it); the level-k state goes through HBM
+        if (P.colB == 32 && !std::getenv("SG_NO_OCT_SPLIT") && !d.parts.empty())
+            d.oct_scratch = dev_alloc<double>(d, d.parts.size() * static_cast<std::size_t>(pbx) * pby * 32 * 32);
         std::vector<double*> rt(static_cast<std::size_t>(nparts_) * P.nslots);
         std::vector<const double*> it(nparts_);
         std::vector<double*> ot(nparts_);
@@ -427,6 +432,7 @@ void Solver::finalize_swept() {
             }
             a.nimp = static_cast<int>(T.imports.size());
             a.nimp_b = T.nimp_b;
+            a.oct_scratch = d.oct_scratch;
             a.lo_parity = std::getenv("SG_NO_SERPENTINE") ? 0 : static_cast<int>(li & 1);
             a.inits = d.d_init[L.cls];
             a.ninit = static_cast<int>(T.inits.size());

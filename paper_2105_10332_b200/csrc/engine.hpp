@@ -50,6 +50,7 @@ struct DeviceCtx {
     std::map<std::pair<int, int>, std::vector<int>> imp_off_host;  // host copy of imp_off's offsets
     std::map<std::pair<int, int>, int*> imp_dense; // (class, slot rotation) -> dense gather table (or null)
     double** d_rec_tab = nullptr;
+    double* oct_scratch = nullptr;  // b32 split Octahedron: level-k state of every instance
     double** d_frames_tab = nullptr;
     const double** d_init_tab = nullptr;
     double** d_out_tab = nullptr;

@@ -47,6 +47,8 @@ struct SweptArgs {
     const int2* imports2;    // {seg << 20 | src, dst}  (same entries, compact)
     const int2* imp_off;     // column kernels: {offset from the instance's slot-0 record, smem slot}
     int nimp_b;              // column kernels: the last nimp_b entries are gather part B
+    double* oct_scratch;     // column kernels, b32: [dev part][bj][bi][row][lane] level-k state between
+                             // the two halves of a split Octahedron (null: one launch)
     const int* imp_dense;    // column kernels, steady classes: [import slot] -> offset from the slot-0 record
     int dense;               // 1: imp_dense covers every import slot (no initial-plane cells)
     int lo_parity;           // column kernels: launch index parity (odd: CTAs walk the instances backwards)
