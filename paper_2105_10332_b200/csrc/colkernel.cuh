@@ -76,6 +76,9 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
     const int half = A.frame * (B / 2);
     const int gh = A.ghost;
     double* S = sm + slot_in_cta * A.smem_doubles;
+    // the second half of a split Octahedron holds only slots [NK, NIMP): its
+    // shared addresses are offset by -NK slots (unsigned arithmetic)
+    constexpr unsigned SOFF = HALF == 2 ? 8u * col::imp_base(KIND, B, KO + 1, YLO) : 0u;
 
     // ---- gather the imports
     // REGS: part A through registers (LDG, then STS: an LDGSTS writes shared
@@ -117,7 +120,7 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
         if (live) {
             const double* ibase = A.rec[part * A.nslots] + ((long)(bj + gh) * A.extw + (bi + gh)) * A.epad;
             const int* tab = A.imp_dense + l;
-            const unsigned s0 = static_cast<unsigned>(__cvta_generic_to_shared(S)) + 8u * l;
+            const unsigned s0 = static_cast<unsigned>(__cvta_generic_to_shared(S)) - SOFF + 8u * l;
             auto part_copy = [&](auto LO, auto HI) {
                 constexpr int lo = decltype(LO)::value, hi = decltype(HI)::value;
                 sfor<(hi - lo + L - 1) / L>([&](auto KI) {
@@ -180,7 +183,7 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
 
     double* dst = A.rec[part * A.nslots + A.my_slot] + ((long)(bj + gh) * A.extw + (bi + gh)) * A.epad;
     const double fx = A.c0, fy = A.c1;
-    const unsigned s_imp = static_cast<unsigned>(__cvta_generic_to_shared(S));
+    const unsigned s_imp = static_cast<unsigned>(__cvta_generic_to_shared(S)) - SOFF;
     unsigned sc[CPL];  // shared address of slot c (c = the lane's column), for COL-mode imports
     double* pc[CPL];   // record address of index c, for COL-mode exports
 #pragma unroll
@@ -592,11 +595,11 @@ inline int env_int(const char* name, int dflt) {
 // default).  The gathers land through L1 (cp.async.ca, the gather tables):
 // with the register-lean steady-state kernels the driver would otherwise
 // pack up to ~28 warps per SM and leave L1 a few KB (b16 YBridge 0.36 vs
-// 0.29 ms, Octahedron 0.73 vs 0.55 ms; profiles/r02_summary.md).
+// 0.29 ms, Octahedron 0.73 vs 0.55 ms; profiles/r02b_summary.md).
 template <int B, int WPC>
 constexpr int target_ctas(int kind) {
     if constexpr (B <= 16) return WPC <= 2 ? 9 : 18 / WPC;  // 18 warps per SM (CPL = 2: 36 instances at WPC 1)
-    else return kind == col::OCT ? 0 : 3;                   // 4-warp CTAs: 12 warps
+    else return kind == col::OCT ? 0 : 4;                   // 4-warp CTAs: 16 warps
 }
 
 template <int B, int CPL, int WPC>
@@ -637,7 +640,19 @@ cudaError_t launch_heat_col_t(const SweptArgs& a, cudaStream_t s) {
             if (a.oct_scratch && (flags == 3 || flags == 7)) {
                 const cudaError_t e = go(swept_heat_col_kernel<B, kd, CPL, WPC, 3 | 16>);
                 if (e != cudaSuccess) return e;
-                return go(swept_heat_col_kernel<B, kd, CPL, WPC, 3 | 32>);
+                // second half: shared memory for its own imports only
+                constexpr int NK = col::imp_base(col::OCT, B, B / 2, 0), NI = col::imp_total(col::OCT, B);
+                static_assert(col::tile_doubles(col::OCT, B) == 0, "no transpose tile in the Octahedron");
+                SweptArgs a2 = a;
+                a2.smem_doubles = NI - NK;
+                const size_t smem2 = static_cast<size_t>(IPC) * a2.smem_doubles * sizeof(double);
+                auto kern2 = swept_heat_col_kernel<B, kd, CPL, WPC, 3 | 32>;
+                if (smem2 > 48 * 1024)
+                    cudaFuncSetAttribute(kern2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+                cudaFuncSetAttribute(kern2, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     static_cast<int>(cudaSharedmemCarveoutDefault));
+                kern2<<<grid, WPC * 32, smem2, s>>>(a2);
+                return cudaGetLastError();
             }
         }
         if (flags == 7) return go(swept_heat_col_kernel<B, kd, CPL, WPC, 7>);
