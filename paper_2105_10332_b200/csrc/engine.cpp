@@ -332,7 +332,8 @@ void Solver::finalize_swept() {
         // each kernel's straight-line code is half as long (instruction
         // fetch bound it); the level-k state goes through HBM
         if (P.colB == 32 && !std::getenv("SG_NO_OCT_SPLIT") && !d.parts.empty())
-            d.oct_scratch = dev_alloc<double>(d, d.parts.size() * static_cast<std::size_t>(pbx) * pby * 32 * 32);
+            d.oct_scratch =
+                dev_alloc<double>(d, d.parts.size() * static_cast<std::size_t>(pbx) * pby * P.colB * P.colB);
         std::vector<double*> rt(static_cast<std::size_t>(nparts_) * P.nslots);
         std::vector<const double*> it(nparts_);
         std::vector<double*> ot(nparts_);

@@ -2,7 +2,8 @@
 
 The launcher picks, per launch, the steady-state kernel with the dense
 slot-indexed gather (FLAGS 3), with the table gather (FLAGS 1), the dense
-gather through registers (FLAGS 7, b32 Octahedron by default) or the general
+gather through registers (FLAGS 7), the Octahedron split into two launches
+(b32, FLAGS bits 4-5; b24 measured no gain) or the general
 kernel with the output / snapshot stash (FLAGS 0), and sizes the
 shared-memory carveout (colkernel.cuh launch_heat_col_t).  The switches are
 read once per process, so each variant runs in its own process; all must
@@ -35,6 +36,7 @@ VARIANTS = {
     "table": {"SG_DENSE_KINDS": "0"},
     "regs": {"SG_REG_KINDS": "31"},
     "carve_default": {"SG_CARVE_OCT": "-1", "SG_CARVE_BR": "-1"},
+    "one_octahedron_launch": {"SG_NO_OCT_SPLIT": "1"},
 }
 
 
