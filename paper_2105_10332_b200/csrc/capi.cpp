@@ -179,6 +179,7 @@ int sg_run(const sg_config* cfg, sg_result* out, char* err, size_t errlen) {
     std::memset(out, 0, sizeof *out);
     return guard(err, errlen, [&] {
         sg::Solver solver(*cfg);
+        solver.set_graph(false);  // one solve: no graph capture inside wall_seconds
         const auto t0 = std::chrono::steady_clock::now();
         solver.reset();
         solver.solve();

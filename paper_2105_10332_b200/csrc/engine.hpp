@@ -95,6 +95,9 @@ class Solver {
     const Setup& setup() const { return setup_; }
     double setup_seconds = 0.0;
     bool profile = false;
+    // a one-shot solve (sg_run) enqueues its launches directly: capturing and
+    // instantiating a CUDA graph costs more than it saves on a single replay
+    void set_graph(bool on) { use_graph_ = use_graph_ && on; }
     bool use_graph_ = true;   // SG_NO_GRAPH=1 disables CUDA graph replay
 
     // distributed (one process per GPU): export this rank's buffers as CUDA
