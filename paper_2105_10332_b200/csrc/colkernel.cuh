@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <vector>
 
 #include "colgeom.hpp"
 #include "devutil.cuh"
@@ -586,6 +587,36 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_col_kernel(const __grid_c
     }
 }
 
+// Function attributes (dynamic shared-memory limit, carveout) set only when
+// they change: the launcher runs once per phase launch, and outside CUDA
+// graphs (one process per GPU) every host call is on the launch path.
+inline void set_attrs(const void* fn, size_t smem, int carve) {
+    struct Attr {
+        const void* fn;
+        int dev;
+        size_t smem;
+        int carve;
+    };
+    static thread_local std::vector<Attr> seen;
+    int dev = 0;
+    cudaGetDevice(&dev);  // attributes are per device context
+    for (Attr& e : seen)
+        if (e.fn == fn && e.dev == dev) {
+            if (smem > e.smem && smem > 48 * 1024) {
+                cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                e.smem = smem;
+            }
+            if (carve != e.carve) {
+                cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+                e.carve = carve;
+            }
+            return;
+        }
+    if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+    seen.push_back({fn, dev, smem > 48 * 1024 ? smem : 48 * 1024, carve});
+}
+
 inline int env_int(const char* name, int dflt) {
     const char* v = std::getenv(name);
     return v ? std::atoi(v) : dflt;
@@ -628,9 +659,8 @@ cudaError_t launch_heat_col_t(const SweptArgs& a, cudaStream_t s) {
     if (a.kind == col::OCT && carve_oct != -2) carve = carve_oct;
     if (bridge && carve_br != -2) carve = carve_br;
     auto go = [&](auto kern) {
-        if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             carve >= 0 ? carve : static_cast<int>(cudaSharedmemCarveoutDefault));
+        set_attrs(reinterpret_cast<const void*>(kern), smem,
+                  carve >= 0 ? carve : static_cast<int>(cudaSharedmemCarveoutDefault));
         kern<<<grid, WPC * 32, smem, s>>>(a);
         return cudaGetLastError();
     };
@@ -647,10 +677,8 @@ cudaError_t launch_heat_col_t(const SweptArgs& a, cudaStream_t s) {
                 a2.smem_doubles = NI - NK;
                 const size_t smem2 = static_cast<size_t>(IPC) * a2.smem_doubles * sizeof(double);
                 auto kern2 = swept_heat_col_kernel<B, kd, CPL, WPC, 3 | 32>;
-                if (smem2 > 48 * 1024)
-                    cudaFuncSetAttribute(kern2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
-                cudaFuncSetAttribute(kern2, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                     static_cast<int>(cudaSharedmemCarveoutDefault));
+                set_attrs(reinterpret_cast<const void*>(kern2), smem2,
+                          static_cast<int>(cudaSharedmemCarveoutDefault));
                 kern2<<<grid, WPC * 32, smem2, s>>>(a2);
                 return cudaGetLastError();
             }

@@ -13,11 +13,11 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/la
     python bench.py --req-steps 140 --steps 1 --warmup 3 --no-cpu --no-extra > $O/launches_bench_r02b.log 2>&1
 python profiles/launch_summary.py $O/launches_r02b.csv > $O/launches_r02b.txt 2>&1
 for B in 16 32; do
-  ncu --set full --clock-control none --import-source on -k regex:swept_heat_col -s 9 -c 3 \
+  ncu --set full --clock-control none --import-source on -k regex:swept_heat_col -s 9 -c 4 \
       -o $O/cyc$B python bench.py --block $B --req-steps 140 --steps 1 --warmup 3 --no-cpu --no-extra \
       > $O/cyc$B.log 2>&1
   python profiles/ncu_json.py $O/cyc$B.ncu-rep > $O/r02b_cycle_b$B.json
-  python profiles/ncu_wavefronts.py $O/cyc$B.ncu-rep 3 > $O/r02b_cycle_b${B}_wavefronts.json
+  python profiles/ncu_wavefronts.py $O/cyc$B.ncu-rep 4 > $O/r02b_cycle_b${B}_wavefronts.json
 done
 python - <<'PY'
 import json
