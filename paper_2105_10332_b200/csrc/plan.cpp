@@ -469,6 +469,11 @@ SweptPlan compile_swept_plan(int b, const Equation& eq, long m, long final_level
             P.overexport += static_cast<long>(formula.size() - exp_mask[kd].size());
             K.epad = static_cast<int>((K.exp_cells.size() + 3) / 4 * 4);
             K.smem_doubles = std::max(1, col::imp_total(kd, b) + col::tile_doubles(kd, b));
+            // per-instance stride = 8 mod 16 doubles: a warp's next instance
+            // starts half a bank row later, so a row load with <= 8 lanes per
+            // instance is one wavefront (b8 +5 %, b16 +0.6 %)
+            if (const char* e = std::getenv("SG_SMEM_PAD"); !(e && e[0] == '0'))
+                K.smem_doubles = (K.smem_doubles + 7) / 16 * 16 + 8;
             K.split = K.nlev;
             K.nexp_early = 0;
             P.max_epad = std::max(P.max_epad, K.epad);
