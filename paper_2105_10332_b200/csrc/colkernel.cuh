@@ -629,8 +629,11 @@ inline int env_int(const char* name, int dflt) {
 // 0.29 ms, Octahedron 0.73 vs 0.55 ms; profiles/r02b_summary.md).
 template <int B, int WPC>
 constexpr int target_ctas(int kind) {
-    if constexpr (B <= 16) return WPC <= 2 ? 9 : 18 / WPC;  // 18 warps per SM (CPL = 2: 36 instances at WPC 1)
-    else return kind == col::OCT ? 0 : 4;                   // 4-warp CTAs: 16 warps
+    if constexpr (B == 16) return WPC <= 2 ? 9 : 18 / WPC;  // 18 warps per SM
+    // 4-warp CTAs (measured carveout sweeps, 4128^2): the bridges want more
+    // warps than the Octahedron (b8 8, b12 10, b24 7, b32 4 CTAs: +2..4 %)
+    if (kind == col::OCT) return B < 16 ? 18 / WPC : 0;
+    return B == 8 ? 8 : B == 12 ? 10 : B == 24 ? 7 : 4;
 }
 
 template <int B, int CPL, int WPC>
