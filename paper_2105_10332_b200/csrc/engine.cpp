@@ -125,8 +125,9 @@ Solver::Solver(const sg_config& cfg, int rank, int world) : cfg_(cfg), rank_(ran
     }
     if (dist()) {
         DeviceCtx& d = devs_[0];
-        flags_ = dev_alloc<unsigned long long>(d, kMaxParts);
-        ck(cudaMemset(flags_, 0, kMaxParts * sizeof(unsigned long long)), "flags");
+        // [kMaxParts] epochs signalled by the ranks + this rank's epoch counter
+        flags_ = dev_alloc<unsigned long long>(d, kMaxParts + 1);
+        ck(cudaMemset(flags_, 0, (kMaxParts + 1) * sizeof(unsigned long long)), "flags");
     }
 
     if (cfg_.engine == SG_SWEPT) {
@@ -830,10 +831,11 @@ double Solver::solve() {
             }
         }
     };
-    // Single-GPU solves without snapshots/profiling are replayed from a CUDA
-    // graph captured on the first solve: every launch of the solve (up to
-    // ~4300 phase launches at 10k steps) goes to the GPU in one call.
-    const bool graphable = !multi && !dist() && !snap && !profile && use_graph_;
+    // Solves on one device per process without snapshots/profiling are
+    // replayed from a CUDA graph captured on the first solve: every launch of
+    // the solve (up to ~4300 phase launches at 10k steps, twice that with the
+    // barriers of one process per GPU) goes to the GPU in one call.
+    const bool graphable = !multi && !snap && !profile && use_graph_;
     if (graphable) {
         DeviceCtx& d = devs_[0];
         if (!graph_exec_) {
@@ -1079,11 +1081,12 @@ void Solver::connect(const unsigned char* blobs, std::size_t per_rank) {
 }
 
 cudaError_t launch_dist_barrier(unsigned long long* const* peer_flags, unsigned long long* my_flags, int world,
-                                int rank, unsigned long long epoch, int* err, cudaStream_t s);
+                                int rank, unsigned long long* counter, int* err, cudaStream_t s);
 
 void Solver::dist_barrier(DeviceCtx& d) {
     ++epoch_;
-    ck(launch_dist_barrier(d_peer_flags_, flags_, world_, rank_, epoch_, d.d_err, d.stream), "dist barrier");
+    ck(launch_dist_barrier(d_peer_flags_, flags_, world_, rank_, flags_ + kMaxParts, d.d_err, d.stream),
+       "dist barrier");
     ++launches_;
 }
 

@@ -681,8 +681,12 @@ __global__ void substep_rects_kernel(int stage, const double* __restrict__ r1, c
 // 60 s without progress it raises bit 1 of the error flag (TransportError)
 // instead of hanging the GPU.
 __global__ void dist_barrier_kernel(unsigned long long* const* peer_flags, unsigned long long* my_flags, int world,
-                                    int rank, unsigned long long epoch, int* err) {
+                                    int rank, unsigned long long* counter, int* err) {
     if (threadIdx.x != 0) return;
+    // the epoch lives on the device (every rank passes the same sequence of
+    // barriers), so a solve's launches can be replayed from a CUDA graph
+    const unsigned long long epoch = *counter + 1;
+    *counter = epoch;
     __threadfence_system();
     for (int q = 0; q < world; ++q) {
         unsigned long long* f = peer_flags[q] + rank;
@@ -820,8 +824,8 @@ long div_selftest(long n, unsigned long long seed, double* xy_bad) {
 }
 
 cudaError_t launch_dist_barrier(unsigned long long* const* peer_flags, unsigned long long* my_flags, int world,
-                                int rank, unsigned long long epoch, int* err, cudaStream_t s) {
-    dist_barrier_kernel<<<1, 32, 0, s>>>(peer_flags, my_flags, world, rank, epoch, err);
+                                int rank, unsigned long long* counter, int* err, cudaStream_t s) {
+    dist_barrier_kernel<<<1, 32, 0, s>>>(peer_flags, my_flags, world, rank, counter, err);
     return cudaGetLastError();
 }
 
