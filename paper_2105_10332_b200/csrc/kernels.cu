@@ -215,11 +215,11 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_kernel(const __grid_const
 // the heat kernel (4 variables per record entry), then every level of the
 // phase runs through euler_rect on shared memory (pressures, shared x/y
 // interface fluxes, update), then the record is scattered.
-template <int MINB>
-__global__ void __launch_bounds__(128, MINB) swept_euler_kernel(const __grid_constant__ SweptArgs A) {
+template <int MINB, int NT = 128, bool FUSED = false>
+__global__ void __launch_bounds__(NT, MINB) swept_euler_kernel(const __grid_constant__ SweptArgs A) {
     extern __shared__ double S[];
     __shared__ const double* sb[kMaxSegs];
-    const int tid = threadIdx.x, T = 128;
+    const int tid = threadIdx.x, T = NT;
     const int inst = blockIdx.x;
     const int part = A.dev_parts[blockIdx.y];
     const int pi = part % A.px, pj = part / A.px;
@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(128, MINB) swept_euler_kernel(const __grid_con
                 }
             }
         };
-        euler_rect(tid, T, Lc.cx0, Lc.cx1, Lc.cy0, Lc.cy1, Q, B, O, ps, fxs, fys, A.c0, stage == 0 ? A.c1 : A.c3,
+        euler_rect<FUSED>(tid, T, Lc.cx0, Lc.cx1, Lc.cy0, Lc.cy1, Q, B, O, ps, fxs, fys, A.c0, stage == 0 ? A.c1 : A.c3,
                    stage == 0 ? A.c2 : A.c4, err);
         if (r == A.split && A.nexp_early > 0) {
             flush(0, A.nexp_early);
@@ -862,11 +862,17 @@ cudaError_t launch_swept(int problem, const SweptArgs& a, cudaStream_t s) {
         // Euler 960^2 b16); 6 (<= 80 registers) since the branch-free flux
         // code: 1.20e10 vs 1.16e10 (7 CTAs, more spills)
         static const int minb = [] { const char* v = std::getenv("SG_EULER_MINB"); return v ? std::atoi(v) : 6; }();
-        auto kern = minb == 5 ? swept_euler_kernel<5> : minb == 6 ? swept_euler_kernel<6> : swept_euler_kernel<7>;
-        if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        // x- and y-interface fluxes in one balanced loop (+3 % at 960^2; 160-
+        // and 192-thread CTAs measured slower: 1.14e10 / 1.05e10 vs 1.23e10)
         dim3 grid(ninst, a.ndev_parts);
-        kern<<<grid, 128, smem, s>>>(a);
-        return cudaGetLastError();
+        auto go = [&](auto kern) {
+            if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            kern<<<grid, 128, smem, s>>>(a);
+            return cudaGetLastError();
+        };
+        if (minb == 5) return go(swept_euler_kernel<5, 128, true>);
+        if (minb == 7) return go(swept_euler_kernel<7, 128, true>);
+        return go(swept_euler_kernel<6, 128, true>);
     }
 }
 
