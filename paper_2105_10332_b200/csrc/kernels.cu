@@ -405,8 +405,8 @@ __global__ void __launch_bounds__(256, MINB) std_euler_kernel(const __grid_const
 //   * out = base - cx*(fe - fw) - cy*(gn - gs) (physics.cpp:131-156), plus the
 //     pushes of partition-edge cells into the neighbours' ghost frames.
 // Non-physical states seen on a path an output cell needs raise the error flag.
-template <int ROWS>
-__global__ void __launch_bounds__(128, 4) std_euler_col_kernel(const __grid_constant__ StdArgs A) {
+template <int ROWS, int MINB = 4>
+__global__ void __launch_bounds__(128, MINB) std_euler_col_kernel(const __grid_constant__ StdArgs A) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int x0 = (blockIdx.x * 4 + warp) * 31;
     const int x = x0 - 1 + lane;
@@ -894,6 +894,16 @@ cudaError_t launch_std(int problem, const StdArgs& a, cudaStream_t s) {
             kern<<<grid, 128, 0, s>>>(a);
             return cudaGetLastError();
         };
+        // large grids (>= 16-row strips, plenty of warps): 5 resident CTAs
+        // at 96 registers (some spills) beat 4 at 128 (4096^2: 2.18e10 vs
+        // 2.08e10); the 960^2 grid keeps 4 (1.81e10 vs 1.76e10)
+        static const int minb = [] { const char* v = std::getenv("SG_EULER_STD_MINB"); return v ? std::atoi(v) : 0; }();
+        if (minb == 5 || (minb == 0 && want_rows >= 16)) {
+            if (want_rows >= 64) return go(std_euler_col_kernel<64, 5>, 64);
+            if (want_rows >= 32) return go(std_euler_col_kernel<32, 5>, 32);
+            if (want_rows >= 16) return go(std_euler_col_kernel<16, 5>, 16);
+            return go(std_euler_col_kernel<8, 5>, 8);
+        }
         if (want_rows >= 64) return go(std_euler_col_kernel<64>, 64);
         if (want_rows >= 32) return go(std_euler_col_kernel<32>, 32);
         if (want_rows >= 16) return go(std_euler_col_kernel<16>, 16);
