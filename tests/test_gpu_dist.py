@@ -167,3 +167,65 @@ def test_bench_torchrun_n_ranks(sg, n):
         s.solve()
         want = sg.fnv1a64(s.fetch().final_field.data)
     assert d["final_fnv1a64"] == want
+
+
+def _worker_repeat(rank, world, port, cfgd, q):
+    """Three solves on one DistSolver: the first captures the rank's launches
+    (phase kernels + epoch barriers) in a CUDA graph, the others replay it."""
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    sys.path.insert(0, str(root))
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import paper_2105_10332_b200 as sg
+        s = sg.DistSolver(sg.SolverConfig(**cfgd))
+        outs = []
+        for _ in range(3):
+            s.reset()
+            s.solve()
+            r = s.gather(0)
+            if r is not None:
+                outs.append((r.final_field.data.copy(), r.final_field.level))
+        s.close()
+        if rank == 0:
+            q.put(("ok", outs))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # noqa: BLE001
+        q.put(("err", repr(e)))
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("engine,problem", [("swept", "heat"), ("standard", "euler")])
+def test_distributed_graph_replay(sg, oracle, engine, problem):
+    """Repeated solves of one process per partition (graph replay with the
+    device-side barrier epoch) stay bitwise equal to the oracle."""
+    if sg.device_count() < 1:
+        pytest.fail("no CUDA device")
+    import torch.multiprocessing as mp
+    nx = 64
+    cfgd = dict(problem=problem, nx=nx, block=16 if problem == "heat" else 8, steps=20, engine=engine,
+                ranks=2, px=2, py=1)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_repeat, args=(r, 2, port, cfgd, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=500)
+    for p in procs:
+        p.join(timeout=120)
+    assert res[0] == "ok", res[1]
+    outs = res[1]
+    assert len(outs) == 3
+    P = oracle.HEAT if problem == "heat" else oracle.EULER
+    init, params = oracle.params(P, nx)
+    want = oracle.standard_solve(P, init, outs[0][1], params)
+    for data, level in outs:
+        assert level == outs[0][1]
+        assert np.array_equal(data, want)
