@@ -210,8 +210,9 @@ void Solver::build_swept() {
     // one instance's phase must fit on chip (levels + Euler flux scratch)
     int inst_smem = 0;
     for (int kd = 0; kd < K_NKINDS; ++kd) inst_smem = std::max(inst_smem, P.kinds[kd].smem_doubles * 8);
-    if (inst_smem > 220 * 1024)
-        fail(SG_EINVAL, "swept: block too large for the on-chip phases (shared memory per instance)");
+    // phases that do not fit on chip (heat b > 48, Euler b > 32) keep their
+    // level storage in HBM (the GM kernels, kernels.cu); allocated in finalize
+    gm_phases_ = inst_smem > 220 * 1024 || std::getenv("SG_FORCE_GM");
 
     if (!snap_path_.empty()) {
         // level l is complete after the last launch computing it; frames are
@@ -332,6 +333,36 @@ void Solver::finalize_swept() {
         // b32: the Octahedron runs as two launches (levels 1..k, k+1..2k) so
         // each kernel's straight-line code is half as long (instruction
         // fetch bound it); the level-k state goes through HBM
+        if (gm_phases_ && !d.parts.empty()) {
+            // per-CTA (Euler: level planes + pressure / flux scratch) or per-warp
+            // (heat, 4 warps per CTA) storage for a persistent grid of <= 4
+            // CTAs per SM, capped at ~8 GB
+            const bool heat = setup_.eq.problem == SG_HEAT;
+            long per = 0;
+            for (int kd = 0; kd < K_NKINDS; ++kd) {
+                const KindLayout& K = P.kinds[kd];
+                long need = K.smem_doubles;
+                if (!heat) {
+                    long ps = 1, fx = 1;
+                    for (int r = 1; r <= K.nlev; ++r) {
+                        const Rect c = K.at(r).comp;
+                        ps = std::max<long>(ps, (c.w() + 4) * (c.h() + 4));
+                        fx = std::max<long>(fx, 4L * std::max(c.h() * (c.w() + 1), (c.h() + 1) * c.w()));
+                    }
+                    need += ((ps + 1) & ~1L) + 2 * ((fx + 1) & ~1L);
+                }
+                per = std::max(per, need);
+            }
+            d.gm_stride = (per + 31) / 32 * 32;
+            const long slots_per_cta = heat ? 4 : 1;
+            const long ninst = static_cast<long>(pbx) * pby;
+            long ctas = std::min<long>((ninst + slots_per_cta - 1) / slots_per_cta, 148L * 4);
+            const long cap = (8L << 30) / (8L * d.gm_stride * slots_per_cta * static_cast<long>(d.parts.size()));
+            ctas = std::max<long>(1, std::min(ctas, cap));
+            d.gm_ctas = static_cast<int>(ctas);
+            d.gm_scratch = dev_alloc<double>(d, static_cast<std::size_t>(ctas * slots_per_cta * d.gm_stride) *
+                                                    d.parts.size());
+        }
         if (P.colB == 32 && !std::getenv("SG_NO_OCT_SPLIT") && !d.parts.empty())
             d.oct_scratch =
                 dev_alloc<double>(d, d.parts.size() * static_cast<std::size_t>(pbx) * pby * P.colB * P.colB);
@@ -435,6 +466,9 @@ void Solver::finalize_swept() {
             a.nimp = static_cast<int>(T.imports.size());
             a.nimp_b = T.nimp_b;
             a.oct_scratch = d.oct_scratch;
+            a.gm_scratch = d.gm_scratch;
+            a.gm_stride = d.gm_stride;
+            a.gm_ctas = d.gm_ctas;
             a.lo_parity = std::getenv("SG_NO_SERPENTINE") ? 0 : static_cast<int>(li & 1);
             a.inits = d.d_init[L.cls];
             a.ninit = static_cast<int>(T.inits.size());
@@ -678,6 +712,7 @@ double Solver::solve() {
     // earlier readers of the record slot a launch overwrites, and its previous
     // writer.
     const bool concurrent = cfg_.engine == SG_SWEPT && !multi && !dist() && !snap && !profile &&
+                            !gm_phases_ &&  // (the GM kernels share one level-storage scratch)
                             !std::getenv("SG_SERIAL_BRIDGES");
     std::vector<int> on_side;
     if (concurrent) {

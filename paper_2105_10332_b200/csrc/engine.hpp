@@ -51,6 +51,9 @@ struct DeviceCtx {
     std::map<std::pair<int, int>, int*> imp_dense; // (class, slot rotation) -> dense gather table (or null)
     double** d_rec_tab = nullptr;
     double* oct_scratch = nullptr;  // b32 split Octahedron: level-k state of every instance
+    double* gm_scratch = nullptr;   // phases too large for shared memory: level storage in HBM
+    long gm_stride = 0;
+    int gm_ctas = 0;
     double** d_frames_tab = nullptr;
     const double** d_init_tab = nullptr;
     double** d_out_tab = nullptr;
@@ -99,6 +102,7 @@ class Solver {
     // instantiating a CUDA graph costs more than it saves on a single replay
     void set_graph(bool on) { use_graph_ = use_graph_ && on; }
     bool use_graph_ = true;   // SG_NO_GRAPH=1 disables CUDA graph replay
+    bool gm_phases_ = false;  // swept phases with their level storage in HBM (blocks too large for smem)
 
     // distributed (one process per GPU): export this rank's buffers as CUDA
     // IPC handles, then map every other rank's and build the kernel tables

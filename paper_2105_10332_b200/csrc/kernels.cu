@@ -48,19 +48,23 @@ namespace {
 //     above `split` (an Octahedron's shrinking half, which gets no imports)
 //     reuse the storage of the dead lower levels, so the lower levels'
 //     exports are flushed first.
-template <int WPC>
+// GM: the phase's level storage lives in a per-warp global-memory scratch
+// (A.gm_scratch, L1/L2-cached) instead of shared memory -- blocks whose
+// phases exceed the 227 KB of shared memory (heat b > 48); a persistent grid
+// walks the instances.  Correct, not fast.
+template <int WPC, bool GM = false>
 __global__ void __launch_bounds__(WPC * 32) swept_heat_kernel(const __grid_constant__ SweptArgs A) {
     extern __shared__ double sm[];
     __shared__ const double* segbase[WPC][kMaxSegs];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ninst = A.pbx * A.pby;
-    const int inst = blockIdx.x * WPC + warp;
-    if (inst >= ninst) return;
+    for (int inst = blockIdx.x * WPC + warp; inst < ninst; inst += GM ? gridDim.x * WPC : ninst) {
     const int part = A.dev_parts[blockIdx.y];
     const int pi = part % A.px, pj = part / A.px;
     const int bi = inst % A.pbx, bj = inst / A.pbx;
     const int half = A.frame * (A.b / 2);
-    double* S = sm + warp * A.smem_doubles;
+    double* S = GM ? A.gm_scratch + (((long)blockIdx.y * gridDim.x + blockIdx.x) * WPC + warp) * A.gm_stride
+                   : sm + warp * A.smem_doubles;
     const double** sb = segbase[warp];
 
     // ---- 1. gather
@@ -70,7 +74,12 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_kernel(const __grid_const
         sb[lane] = A.rec[part * A.nslots + sg.slot] + ext * sg.epad;
     }
     __syncwarp();
-    {
+    if (GM) {
+        for (int i = lane; i < A.nimp; i += 32) {
+            const int2 e = ldg_keep(&A.imports2[i]);
+            S[e.y] = sb[e.x >> 20][e.x & 0xFFFFF];
+        }
+    } else {
         const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(S));
         int i = lane;
         for (; i + 96 < A.nimp; i += 128) {
@@ -209,18 +218,25 @@ __global__ void __launch_bounds__(WPC * 32) swept_heat_kernel(const __grid_const
     }
     // ---- 3. scatter the rest of the record
     if (A.nexp > A.nexp_early) flush(A.nexp_early, A.nexp);
+    __syncwarp();  // (GM: the next instance reuses the scratch)
+    }
 }
 
 // Euler phase kernel: one CTA (128 threads) per block instance.  Gather as
 // the heat kernel (4 variables per record entry), then every level of the
 // phase runs through euler_rect on shared memory (pressures, shared x/y
 // interface fluxes, update), then the record is scattered.
-template <int MINB, int NT = 128, bool FUSED = false>
+// GM: level storage and flux scratch in a per-CTA global-memory scratch
+// (Euler b > 32), a persistent grid walking the instances (see the heat
+// kernel above).
+template <int MINB, int NT = 128, bool FUSED = false, bool GM = false>
 __global__ void __launch_bounds__(NT, MINB) swept_euler_kernel(const __grid_constant__ SweptArgs A) {
-    extern __shared__ double S[];
+    extern __shared__ double Ssm[];
     __shared__ const double* sb[kMaxSegs];
     const int tid = threadIdx.x, T = NT;
-    const int inst = blockIdx.x;
+    const int ninst = A.pbx * A.pby;
+    for (int inst = blockIdx.x; inst < ninst; inst += GM ? gridDim.x : ninst) {
+    double* S = GM ? A.gm_scratch + ((long)blockIdx.y * gridDim.x + blockIdx.x) * A.gm_stride : Ssm;
     const int part = A.dev_parts[blockIdx.y];
     const int pi = part % A.px, pj = part / A.px;
     const int bi = inst % A.pbx, bj = inst / A.pbx;
@@ -236,7 +252,15 @@ __global__ void __launch_bounds__(NT, MINB) swept_euler_kernel(const __grid_cons
         sb[tid] = A.rec[part * A.nslots + sg.slot] + ext * 4 * sg.epad;
     }
     __syncthreads();
-    {
+    if (GM) {
+        for (int i = tid; i < A.nimp; i += T) {
+            const int4 e = __ldg(&A.imports[i]);
+            const int ep = A.segs[e.x].epad;
+            const double* g = sb[e.x] + e.y;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) S[e.z + v * e.w] = g[v * ep];
+        }
+    } else {
         const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(S));
         for (int i = tid; i < A.nimp; i += T) {
             const int4 e = __ldg(&A.imports[i]);
@@ -328,6 +352,8 @@ __global__ void __launch_bounds__(NT, MINB) swept_euler_kernel(const __grid_cons
     }
     if (A.nexp > A.nexp_early) flush(A.nexp_early, A.nexp);
     if (err) *A.err = 1;
+    __syncthreads();  // (GM: the next instance reuses the scratch)
+    }
 }
 
 // Standard Euler step on a TX x TY output tile per CTA: the cross-shaped
@@ -842,6 +868,16 @@ cudaError_t launch_swept(int problem, const SweptArgs& a, cudaStream_t s) {
     if (problem == 0 && a.colB == 32) return launch_heat_col32(a, s);
     if (problem == 0 && a.colB == 12) return launch_heat_col12(a, s);
     if (problem == 0 && a.colB == 24) return launch_heat_col24(a, s);
+    if (problem == 0 && a.gm_scratch) {
+        dim3 grid(a.gm_ctas, a.ndev_parts);
+        swept_heat_kernel<4, true><<<grid, 128, 0, s>>>(a);
+        return cudaGetLastError();
+    }
+    if (problem == 1 && a.gm_scratch) {
+        dim3 grid(a.gm_ctas, a.ndev_parts);
+        swept_euler_kernel<4, 128, true, true><<<grid, 128, 0, s>>>(a);
+        return cudaGetLastError();
+    }
     if (problem == 0) {
         const size_t per_inst = static_cast<size_t>(a.smem_doubles) * sizeof(double);
         auto go = [&](auto kern, int wpc) {

@@ -47,6 +47,9 @@ struct SweptArgs {
     const int2* imports2;    // {seg << 20 | src, dst}  (same entries, compact)
     const int2* imp_off;     // column kernels: {offset from the instance's slot-0 record, smem slot}
     int nimp_b;              // column kernels: the last nimp_b entries are gather part B
+    double* gm_scratch;      // phases too large for shared memory: per-CTA (Euler) / per-warp (heat)
+    long gm_stride;          // level storage in global memory, gm_stride doubles each (null: shared)
+    int gm_ctas;             // persistent grid of the GM kernels
     double* oct_scratch;     // column kernels, b32: [dev part][bj][bi][row][lane] level-k state between
                              // the two halves of a split Octahedron (null: one launch)
     const int* imp_dense;    // column kernels, steady classes: [import slot] -> offset from the slot-0 record
