@@ -212,7 +212,11 @@ void Solver::build_swept() {
     for (int kd = 0; kd < K_NKINDS; ++kd) inst_smem = std::max(inst_smem, P.kinds[kd].smem_doubles * 8);
     // phases that do not fit on chip (heat b > 48, Euler b > 32) keep their
     // level storage in HBM (the GM kernels, kernels.cu); allocated in finalize
-    gm_phases_ = inst_smem > 220 * 1024 || std::getenv("SG_FORCE_GM");
+    // Euler: also when fewer than 3 instances would fit an SM's shared memory
+    // -- the GM kernels then run 4 CTAs per SM with the levels in L1/L2 and
+    // win (960^2: b32 1.03e10 vs 6.8e9 in shared memory; b24 0.98e10 vs 1.01e10)
+    gm_phases_ = inst_smem > 220 * 1024 || (setup_.eq.problem != SG_HEAT && inst_smem > 76 * 1024) ||
+                 std::getenv("SG_FORCE_GM");
 
     if (!snap_path_.empty()) {
         // level l is complete after the last launch computing it; frames are
