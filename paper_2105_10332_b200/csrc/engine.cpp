@@ -215,8 +215,10 @@ void Solver::build_swept() {
     // Euler: also when fewer than 3 instances would fit an SM's shared memory
     // -- the GM kernels then run 4 CTAs per SM with the levels in L1/L2 and
     // win (960^2: b32 1.03e10 vs 6.8e9 in shared memory; b24 0.98e10 vs 1.01e10)
+    // Heat: when fewer than 2 instances fit (4160^2 b52: 1.21e11 in GM mode vs
+    // 6.7e10 in shared memory; b40 1.15e11 vs 1.18e11)
     gm_phases_ = inst_smem > 220 * 1024 || (setup_.eq.problem != SG_HEAT && inst_smem > 76 * 1024) ||
-                 std::getenv("SG_FORCE_GM");
+                 (setup_.eq.problem == SG_HEAT && inst_smem > 114 * 1024) || std::getenv("SG_FORCE_GM");
 
     if (!snap_path_.empty()) {
         // level l is complete after the last launch computing it; frames are
