@@ -700,16 +700,17 @@ cudaError_t launch_heat_col_t(const SweptArgs& a, cudaStream_t s) {
     }
 }
 // One column (row) per lane: two per lane halves the shuffles but doubles the
-// live registers (Oct b16: 182 vs 106), and the lost occupancy costs more
-// (Oct launch 0.82 vs 0.62 ms, profiles/r01_summary.md).
+// shared memory and registers per warp, and each memory instruction spans
+// four instances' records (steady-state b16 Octahedron 0.88 vs 0.55 ms,
+// DESIGN.md §4).
 template <int B>
 cudaError_t launch_heat_col(const SweptArgs& a, cudaStream_t s) {
     // 4 warps per CTA on big grids; single-warp CTAs when there are too few
     // instances to fill the 148 SMs otherwise (the paper's 320^2..1120^2 grids)
     if constexpr (B == 16)
         if (a.pbx * a.pby * a.ndev_parts < 2 * 4 * 148 * 8) return launch_heat_col_t<B, 1, 1>(a, s);
-    // b16: 2-warp CTAs (finer-grained residency: 18 instead of 16 warps per
-    // SM at ~100 registers; 3.69e11 vs 3.65e11 (4 warps) and 3.61e11 (8))
+    // b16: 2-warp CTAs (finer-grained residency; 4- and 8-warp CTAs measured
+    // 0.58 / 0.63 vs 0.56 ms for the steady-state Octahedron)
     if constexpr (B == 16) {
         return launch_heat_col_t<B, 1, 2>(a, s);
     }
