@@ -32,9 +32,15 @@ def test_library_is_sm100a_and_fmad_free():
     out = subprocess.run(["cuobjdump", "--list-elf", str(so)], capture_output=True, text=True).stdout
     assert "sm_100a" in out
     sass = subprocess.run(["cuobjdump", "-sass", str(so)], capture_output=True, text=True).stdout
-    # -fmad=false: the stencil arithmetic never contracts (DFMA only inside IEEE div/sqrt sequences)
-    heat = sass.split("swept_heat_kernel")[1].split("Function :")[0] if "swept_heat_kernel" in sass else ""
-    assert heat and "DFMA" not in heat
+    # -fmad=false: the heat stencil never contracts (DFMA appears only inside
+    # the Euler kernels' IEEE div/sqrt sequences) -- every heat kernel
+    # instantiation: the register tiles (every block size, kind and variant),
+    # the table-driven phase kernel (shared-memory and GM modes) and the step
+    funcs = sass.split("Function : ")[1:]
+    heat = [f for f in funcs if "heat" in f.split("\n", 1)[0]]
+    assert len(heat) >= 50, len(heat)
+    bad = [f.split("\n", 1)[0] for f in heat if "DFMA" in f]
+    assert not bad, bad[:5]
 
 
 def test_no_cpu_fallback_without_gpu(sg):
