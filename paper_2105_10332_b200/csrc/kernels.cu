@@ -677,8 +677,14 @@ __global__ void substep_rects_kernel(int stage, const double* __restrict__ r1, c
     const long total = prefix[nrects];
     const long pl = (long)nx * ny;
     for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < total; c += (long)gridDim.x * blockDim.x) {
-        int ri = 0;
-        while (prefix[ri + 1] <= c) ++ri;
+        // rectangle of cell c: the last ri with prefix[ri] <= c (binary search)
+        int lo = 0, hi = nrects - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (prefix[mid] <= c) lo = mid;
+            else hi = mid - 1;
+        }
+        const int ri = lo;
         const int x0 = rects[4 * ri], w = rects[4 * ri + 1] - x0, y0 = rects[4 * ri + 2];
         const long rem = c - prefix[ri];
         const int x = x0 + (int)(rem % w), y = y0 + (int)(rem / w);
