@@ -632,7 +632,8 @@ constexpr int target_ctas(int kind) {
     if constexpr (B == 16) return WPC <= 2 ? 9 : 18 / WPC;  // 18 warps per SM
     // 4-warp CTAs (measured carveout sweeps, 4128^2): the bridges want more
     // warps than the Octahedron (b8 8, b12 10, b24 7, b32 4 CTAs: +2..4 %)
-    if (kind == col::OCT) return B < 16 ? 18 / WPC : 0;
+    // (b24: the first half of the split Octahedron, 4 CTAs: 0.295 vs 0.315 ms)
+    if (kind == col::OCT) return B < 16 ? 18 / WPC : B == 24 ? 4 : 0;
     return B == 8 ? 8 : B == 12 ? 10 : B == 24 ? 7 : 4;
 }
 
@@ -669,7 +670,7 @@ cudaError_t launch_heat_col_t(const SweptArgs& a, cudaStream_t s) {
     };
     auto pick = [&](auto K) {
         constexpr int kd = decltype(K)::value;
-        if constexpr (B == 32 && kd == col::OCT && CPL == 1) {
+        if constexpr (B >= 24 && kd == col::OCT && CPL == 1) {
             if (a.oct_scratch && (flags == 3 || flags == 7)) {
                 const cudaError_t e = go(swept_heat_col_kernel<B, kd, CPL, WPC, 3 | 16>);
                 if (e != cudaSuccess) return e;

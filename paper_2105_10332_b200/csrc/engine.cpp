@@ -336,7 +336,7 @@ void Solver::finalize_swept() {
             d.d_imp.push_back(dev_upload(d, im));
             d.d_init.push_back(dev_upload(d, in));
         }
-        // b32: the Octahedron runs as two launches (levels 1..k, k+1..2k) so
+        // b24 / b32: the Octahedron runs as two launches (levels 1..k, k+1..2k) so
         // each kernel's straight-line code is half as long (instruction
         // fetch bound it); the level-k state goes through HBM
         if (gm_phases_ && !d.parts.empty()) {
@@ -369,7 +369,7 @@ void Solver::finalize_swept() {
             d.gm_scratch = dev_alloc<double>(d, static_cast<std::size_t>(ctas * slots_per_cta * d.gm_stride) *
                                                     d.parts.size());
         }
-        if (P.colB == 32 && !std::getenv("SG_NO_OCT_SPLIT") && !d.parts.empty())
+        if (P.colB >= 24 && !std::getenv("SG_NO_OCT_SPLIT") && !d.parts.empty())
             d.oct_scratch =
                 dev_alloc<double>(d, d.parts.size() * static_cast<std::size_t>(pbx) * pby * P.colB * P.colB);
         std::vector<double*> rt(static_cast<std::size_t>(nparts_) * P.nslots);

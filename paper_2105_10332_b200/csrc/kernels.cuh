@@ -50,7 +50,7 @@ struct SweptArgs {
     double* gm_scratch;      // phases too large for shared memory: per-CTA (Euler) / per-warp (heat)
     long gm_stride;          // level storage in global memory, gm_stride doubles each (null: shared)
     int gm_ctas;             // persistent grid of the GM kernels
-    double* oct_scratch;     // column kernels, b32: [dev part][bj][bi][row][lane] level-k state between
+    double* oct_scratch;     // column kernels, b24 / b32: [dev part][bj][bi][row][lane] level-k state between
                              // the two halves of a split Octahedron (null: one launch)
     const int* imp_dense;    // column kernels, steady classes: [import slot] -> offset from the slot-0 record
     int dense;               // 1: imp_dense covers every import slot (no initial-plane cells)
